@@ -1,0 +1,163 @@
+/*
+ * bf.h - C ABI of the B200 (sm_100a) joint-acceleration bilateral filter library (libbf.so).
+ *
+ * Implements the hot path of "Speeding up the Bilateral Filter: A Joint Acceleration Way"
+ * (Dai, Yuan, Zhang; arXiv 1803.00004). Citations "P:n" are lines of the paper's LaTeX source
+ * (PAPER.md); "Q<n>" are the readings of the paper listed in DESIGN.md / SURVEY.md 8(c).
+ *
+ * The bilateral filter (eq:BF)
+ *     out(x) = sum_y K_s(|x-y|) K_r(I(x)-I(y)) I(y) / sum_y K_s(|x-y|) K_r(I(x)-I(y))
+ * is evaluated as the paper's box-filter expansion (eq:numerator_2D_box_N_terms):
+ *   - K_r is replaced by its best N-term cosine expansion on [-D, D] (the Case 1
+ *     substitution T_{r_i} = D of P:1205/P:1215-1217, Q1, which makes the z-window of the
+ *     dimension promotion cover every intensity so the 3-D box filters collapse to 2-D);
+ *   - the truncated K_s is replaced by its best N_s-term 2-D Haar expansion on
+ *     [-(r+1/2), r+1/2]^2 (Q8/Q9), lowered to box filters (Appendix A);
+ *   - every cosine term k contributes the channels cos(w_k I), sin(w_k I), I cos(w_k I),
+ *     I sin(w_k I), which are box-filtered and recombined with the per-pixel factors
+ *     a_k cos(w_k I(x)), a_k sin(w_k I(x)) (Q17); out = num / den.
+ *
+ * All functions are thread-safe. A plan is immutable after creation and may be used
+ * concurrently by several bf_apply calls on different streams.
+ */
+#ifndef BF_H_
+#define BF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BF_API __attribute__((visibility("default")))
+#else
+#define BF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Opaque, library-owned, immutable plan (host memory only). */
+typedef struct bf_plan bf_plan;
+
+/* CUDA stream handle as an opaque pointer (a cudaStream_t; NULL = the legacy default stream). */
+typedef void* bf_stream;
+
+typedef enum {
+  BF_OK = 0,
+  BF_ERR_INVALID_ARG = 1,   /* NULL pointer, non-positive size, sigma <= 0, N < 1, ...       */
+  BF_ERR_UNSUPPORTED = 2,   /* unknown kernel kind, or a plan shape the GPU path lacks       */
+  BF_ERR_NO_MEMORY = 3,     /* host allocation failed                                        */
+  BF_ERR_CUDA = 4,          /* a CUDA launch or runtime call failed (no device sync is done)  */
+  BF_ERR_NUMERIC = 5        /* the fitter produced no usable term (e.g. all coefficients 0)  */
+} bf_status;
+
+/* Spatial kernel K_s: isotropic Gaussian exp(-(u^2+v^2)/2 sigma_s^2) or a box,
+ * truncated to the square |u|,|v| <= radius (Q9). */
+typedef enum { BF_SPATIAL_GAUSSIAN = 0, BF_SPATIAL_BOX = 1 } bf_spatial_kind;
+
+/* Range kernel K_r: Gaussian exp(-t^2/2 sigma_r^2) (sigma_r = +INFINITY gives
+ * K_r == 1), or the Tukey biweight (1-(t/sigma_r)^2)^2 for |t| <= sigma_r, else 0 (Q22). */
+typedef enum { BF_RANGE_GAUSSIAN = 0, BF_RANGE_TUKEY = 1 } bf_range_kind;
+
+/* Input pixel type; the output is always float32. */
+typedef enum { BF_IN_U8 = 0, BF_IN_F32 = 1 } bf_input_dtype;
+
+typedef struct {
+  double intensity_max;  /* D: inputs must lie in [0, D] (not checked on the device); default 255 */
+  int n_spatial_terms;   /* N_s, the best-N_s Haar terms of K_s; default 9 (Q15)        */
+  int input_dtype;       /* bf_input_dtype; default BF_IN_F32                                   */
+  int m_factor;          /* candidate count M = m_factor * N for the range fit; def 20 */
+  int haar_levels;       /* Haar levels j <= J considered for K_s; default 4           */
+} bf_plan_options;
+
+/* Maximum N (range terms) and N_s (spatial terms) accepted by bf_plan_create. */
+#define BF_MAX_TERMS 32
+#define BF_MAX_SPATIAL_TERMS 64
+/* Maximum boxes per axis of the separable spatial factor the GPU path runs. */
+#define BF_MAX_AXIS_BOXES 4
+
+/* Fills *opt with the defaults listed above. */
+BF_API void bf_plan_options_default(bf_plan_options* opt);
+
+/*
+ * Fits the expansion coefficients on the host (a one-off cost; Table I):
+ *   range:   a_0 = 1/(2D) int_{-D}^{D} K_r,  a_k = 1/D int K_r(t) cos(pi k t / D) dt
+ *            (P:204-208 with T = D), k < M = m_factor * n_terms; the n_terms largest |a_k|
+ *            (ties to the smaller k, zeros pruned: Q4/Q6/Q7);
+ *   spatial: 2-D Haar coefficients (eq:Haar_2D_coefficients) with levels <= J,
+ *            best n_spatial_terms (ties by canonical order), lowered to boxes on integer
+ *            offsets with half-open cells (Q11), factored into separable 1-D box filters.
+ * Arguments: ks, kr kernel kinds; sigma_s > 0 (ignored for BF_SPATIAL_BOX); sigma_r > 0
+ * (may be +INFINITY for the Gaussian); radius >= 0 (spatial truncation r, T_s = r + 1/2);
+ * n_terms in [1, BF_MAX_TERMS]; opt may be NULL (defaults).
+ * On success *out receives a new plan owned by the caller (free with bf_plan_destroy).
+ * On failure *out is set to NULL and an error code is returned; no partial state remains.
+ */
+BF_API bf_status bf_plan_create(bf_plan** out, int ks, int kr, double sigma_s, double sigma_r, int radius,
+                                int n_terms, const bf_plan_options* opt);
+
+/* Releases a plan. NULL is a no-op. Returns BF_OK. */
+BF_API bf_status bf_plan_destroy(bf_plan* plan);
+
+/* Plan contents, for inspection and cross-checking against an independent fitter. */
+typedef struct {
+  int n_terms_eff;                           /* N_eff <= N after pruning zero coefficients     */
+  int k[BF_MAX_TERMS];                       /* selected frequencies (ascending)               */
+  double a[BF_MAX_TERMS];                    /* their coefficients a_k                         */
+  double T_range;                            /* T of the cosine basis (= D)                    */
+  int n_spatial_eff;                         /* selected 2-D Haar terms                        */
+  int sp_family[BF_MAX_SPATIAL_TERMS];       /* 0 phi.phi, 1 phi(x)psi(y), 2 psi(x)phi(y), 3 psi.psi */
+  int sp_j1[BF_MAX_SPATIAL_TERMS], sp_k1[BF_MAX_SPATIAL_TERMS];   /* x factor (j,k); -1,0 = phi */
+  int sp_j2[BF_MAX_SPATIAL_TERMS], sp_k2[BF_MAX_SPATIAL_TERMS];   /* y factor (j,k); -1,0 = phi */
+  double sp_coef[BF_MAX_SPATIAL_TERMS];      /* c_j of the selected terms                      */
+  int separable;                             /* 1 if K~_s = fx(u) fy(v) (GPU path supported)  */
+  int nbx, nby;                              /* boxes per axis of the separable factors        */
+  int box_lo_x[BF_MAX_AXIS_BOXES], box_hi_x[BF_MAX_AXIS_BOXES];  /* column offsets, inclusive  */
+  double box_w_x[BF_MAX_AXIS_BOXES];
+  int box_lo_y[BF_MAX_AXIS_BOXES], box_hi_y[BF_MAX_AXIS_BOXES];  /* row offsets, inclusive     */
+  double box_w_y[BF_MAX_AXIS_BOXES];
+  int radius;                                /* spatial truncation radius r                    */
+  double intensity_max;                      /* D                                              */
+  int input_dtype;                           /* bf_input_dtype                                 */
+} bf_plan_info;
+
+/* Copies the plan contents into *info. */
+BF_API bf_status bf_plan_get_info(const bf_plan* plan, bf_plan_info* info);
+
+/*
+ * Filters one H x W image on the GPU: d_in is a device pointer to a dense row-major image of
+ * the plan's input dtype (pitch W elements), d_out a device pointer to H*W float32 (pitch W).
+ * The caller owns both buffers and the stream; they must not alias. The work is enqueued
+ * asynchronously on `stream` (no host synchronisation, no device allocation, so the call is
+ * CUDA-graph capturable); launch errors are returned as BF_ERR_CUDA, faults appear at the
+ * caller's next synchronisation. Pixels outside the image contribute nothing (Q16). Pixels
+ * whose approximated denominator is <= 0 or not finite get out = I(x) (Q18). The result is
+ * deterministic (fixed reduction order, exact integer box sums, no atomics).
+ * Returns BF_ERR_INVALID_ARG for NULL pointers, H or W <= 0, H*W overflow or d_in == d_out;
+ * BF_ERR_UNSUPPORTED if the plan's spatial factorisation is not separable.
+ */
+BF_API bf_status bf_apply(const bf_plan* plan, const void* d_in, float* d_out, int H, int W, bf_stream stream);
+
+/*
+ * Filters n_frames independent H x W frames stored back to back (frame f at d_in + f*H*W
+ * elements, likewise d_out) in one launch (NEXT f4 of the survey; used for BASELINE cfg3).
+ */
+BF_API bf_status bf_apply_batched(const bf_plan* plan, const void* d_in, float* d_out, int n_frames, int H, int W,
+                           bf_stream stream);
+
+/* Host-to-host convenience for end-to-end timing: copies h_in (host) to the device, filters,
+ * copies the result back into h_out (host) and synchronises `stream`. Device buffers come
+ * from a library-owned cache keyed by size (grown on demand, freed at exit). */
+BF_API bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float* h_out, int H, int W, bf_stream stream);
+
+/* Static string for a status code. */
+BF_API const char* bf_status_string(bf_status s);
+
+/* Library version string ("bf-b200 <semver>"). */
+BF_API const char* bf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BF_H_ */

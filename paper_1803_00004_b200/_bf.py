@@ -1,0 +1,169 @@
+"""ctypes binding of libbf.so (include/bf.h). Argument marshalling only: every step of the
+filter runs inside the library (host fitter + sm_100a kernels). There is no CPU fallback: if
+the library is missing this module raises at import."""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbf.so")
+
+BF_OK, BF_ERR_INVALID_ARG, BF_ERR_UNSUPPORTED, BF_ERR_NO_MEMORY, BF_ERR_CUDA, BF_ERR_NUMERIC = range(6)
+BF_SPATIAL_GAUSSIAN, BF_SPATIAL_BOX = 0, 1
+BF_RANGE_GAUSSIAN, BF_RANGE_TUKEY = 0, 1
+BF_IN_U8, BF_IN_F32 = 0, 1
+BF_MAX_TERMS = 32
+BF_MAX_SPATIAL_TERMS = 64
+BF_MAX_AXIS_BOXES = 4
+
+SPATIAL = {"gaussian": BF_SPATIAL_GAUSSIAN, "box": BF_SPATIAL_BOX}
+RANGE = {"gaussian": BF_RANGE_GAUSSIAN, "tukey": BF_RANGE_TUKEY}
+
+#: every symbol include/bf.h declares (checked by tests/test_abi.py)
+EXPORTS = ("bf_plan_options_default", "bf_plan_create", "bf_plan_destroy", "bf_plan_get_info", "bf_apply",
+           "bf_apply_batched", "bf_apply_host", "bf_status_string", "bf_version")
+
+
+class PlanOptions(C.Structure):
+    _fields_ = [("intensity_max", C.c_double), ("n_spatial_terms", C.c_int), ("input_dtype", C.c_int),
+                ("m_factor", C.c_int), ("haar_levels", C.c_int)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [
+        ("n_terms_eff", C.c_int), ("k", C.c_int * BF_MAX_TERMS), ("a", C.c_double * BF_MAX_TERMS),
+        ("T_range", C.c_double), ("n_spatial_eff", C.c_int),
+        ("sp_family", C.c_int * BF_MAX_SPATIAL_TERMS),
+        ("sp_j1", C.c_int * BF_MAX_SPATIAL_TERMS), ("sp_k1", C.c_int * BF_MAX_SPATIAL_TERMS),
+        ("sp_j2", C.c_int * BF_MAX_SPATIAL_TERMS), ("sp_k2", C.c_int * BF_MAX_SPATIAL_TERMS),
+        ("sp_coef", C.c_double * BF_MAX_SPATIAL_TERMS),
+        ("separable", C.c_int), ("nbx", C.c_int), ("nby", C.c_int),
+        ("box_lo_x", C.c_int * BF_MAX_AXIS_BOXES), ("box_hi_x", C.c_int * BF_MAX_AXIS_BOXES),
+        ("box_w_x", C.c_double * BF_MAX_AXIS_BOXES),
+        ("box_lo_y", C.c_int * BF_MAX_AXIS_BOXES), ("box_hi_y", C.c_int * BF_MAX_AXIS_BOXES),
+        ("box_w_y", C.c_double * BF_MAX_AXIS_BOXES),
+        ("radius", C.c_int), ("intensity_max", C.c_double), ("input_dtype", C.c_int),
+    ]
+
+
+class BFError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {lib().bf_status_string(status).decode()}")
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1803_00004_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.bf_plan_options_default.argtypes = [C.POINTER(PlanOptions)]
+        L.bf_plan_options_default.restype = None
+        L.bf_plan_create.argtypes = [C.POINTER(P), C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                     C.POINTER(PlanOptions)]
+        L.bf_plan_create.restype = C.c_int
+        L.bf_plan_destroy.argtypes = [P]
+        L.bf_plan_destroy.restype = C.c_int
+        L.bf_plan_get_info.argtypes = [P, C.POINTER(PlanInfo)]
+        L.bf_plan_get_info.restype = C.c_int
+        L.bf_apply.argtypes = [P, P, P, C.c_int, C.c_int, P]
+        L.bf_apply.restype = C.c_int
+        L.bf_apply_batched.argtypes = [P, P, P, C.c_int, C.c_int, C.c_int, P]
+        L.bf_apply_batched.restype = C.c_int
+        L.bf_apply_host.argtypes = [P, P, P, C.c_int, C.c_int, P]
+        L.bf_apply_host.restype = C.c_int
+        L.bf_status_string.argtypes = [C.c_int]
+        L.bf_status_string.restype = C.c_char_p
+        L.bf_version.argtypes = []
+        L.bf_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(status: int, where: str) -> None:
+    if status != BF_OK:
+        raise BFError(status, where)
+
+
+class Plan:
+    """A bf_plan (host-fitted coefficients). Mirrors bf_plan_create's arguments."""
+
+    def __init__(self, spatial: str = "gaussian", range_kind: str = "gaussian", sigma_s: float = 3.0,
+                 sigma_r: float = 30.0, radius: int = 9, n_terms: int = 8, intensity_max: float = 255.0,
+                 n_spatial: int = 9, input_dtype: str = "f32", m_factor: int = 20, haar_levels: int = 4):
+        L = lib()
+        opt = PlanOptions()
+        L.bf_plan_options_default(C.byref(opt))
+        opt.intensity_max = float(intensity_max)
+        opt.n_spatial_terms = int(n_spatial)
+        opt.input_dtype = BF_IN_U8 if input_dtype in ("u8", "uint8") else BF_IN_F32
+        opt.m_factor = int(m_factor)
+        opt.haar_levels = int(haar_levels)
+        h = C.c_void_p()
+        st = L.bf_plan_create(C.byref(h), SPATIAL[spatial], RANGE[range_kind], float(sigma_s), float(sigma_r),
+                              int(radius), int(n_terms), C.byref(opt))
+        _check(st, "bf_plan_create")
+        self._h = h
+        self.input_dtype = "u8" if opt.input_dtype == BF_IN_U8 else "f32"
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def info(self) -> dict:
+        inf = PlanInfo()
+        _check(lib().bf_plan_get_info(self._h, C.byref(inf)), "bf_plan_get_info")
+        n, ns = inf.n_terms_eff, inf.n_spatial_eff
+        return dict(
+            k=list(inf.k[:n]), a=list(inf.a[:n]), T_range=inf.T_range,
+            spatial_terms=[(inf.sp_family[i], inf.sp_j1[i], inf.sp_k1[i], inf.sp_j2[i], inf.sp_k2[i], inf.sp_coef[i])
+                           for i in range(ns)],
+            separable=bool(inf.separable),
+            boxes_x=[(inf.box_lo_x[i], inf.box_hi_x[i], inf.box_w_x[i]) for i in range(inf.nbx)],
+            boxes_y=[(inf.box_lo_y[i], inf.box_hi_y[i], inf.box_w_y[i]) for i in range(inf.nby)],
+            radius=inf.radius, intensity_max=inf.intensity_max,
+            input_dtype="u8" if inf.input_dtype == BF_IN_U8 else "f32")
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().bf_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def apply(plan: Plan, d_in: int, d_out: int, H: int, W: int, stream: int = 0) -> None:
+    """bf_apply on raw device pointers (ints) and a raw cudaStream_t (int)."""
+    _check(lib().bf_apply(plan.handle, C.c_void_p(d_in), C.c_void_p(d_out), int(H), int(W), C.c_void_p(stream)),
+           "bf_apply")
+
+
+def apply_batched(plan: Plan, d_in: int, d_out: int, n_frames: int, H: int, W: int, stream: int = 0) -> None:
+    _check(lib().bf_apply_batched(plan.handle, C.c_void_p(d_in), C.c_void_p(d_out), int(n_frames), int(H), int(W),
+                                  C.c_void_p(stream)), "bf_apply_batched")
+
+
+def apply_host(plan: Plan, h_in: int, h_out: int, H: int, W: int, stream: int = 0) -> None:
+    """bf_apply_host on raw host pointers (copies in, filters, copies out, synchronises)."""
+    _check(lib().bf_apply_host(plan.handle, C.c_void_p(h_in), C.c_void_p(h_out), int(H), int(W), C.c_void_p(stream)),
+           "bf_apply_host")
+
+
+def version() -> str:
+    return lib().bf_version().decode()
+
+
+def is_inf(x: float) -> bool:
+    return math.isinf(x)

@@ -1,0 +1,181 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded
+inputs. Tolerance (BASELINE.json north_star): max-abs <= 1e-3 and RMSE <= 1e-4 on intensities
+scaled to [0, 255]. Full images at sizes the oracle finishes in seconds (several strips/bands
+and ragged tails), sampled pixels at the configs' full sizes, and edge cases."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import bf, fit
+from synth import CONFIGS, config_input, config_params
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS = 1e-3
+RMSE = 1e-4
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import torch
+    from paper_1803_00004_b200 import build
+    build.build()
+    import paper_1803_00004_b200 as pkg
+    assert torch.cuda.is_available()
+    return pkg, torch
+
+
+def make_plans(pkg, params, dtype, **over):
+    p = dict(params)
+    p.update(over)
+    gp = pkg.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"], sigma_r=p["sigma_r"],
+                  radius=p["radius"], n_terms=p["n_terms"], intensity_max=p["intensity_max"],
+                  n_spatial=p.get("n_spatial", 9), input_dtype="u8" if dtype == np.uint8 else "f32")
+    op = fit.make_plan(**p)
+    return gp, op
+
+
+def run_gpu(pkg, torch, plan, img):
+    t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+    out = pkg.bilateral_filter(plan, t)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+def assert_parity(got, ref, D, what=""):
+    e = np.abs(got - ref) * (255.0 / D)
+    mx, rm = float(e.max()), float(np.sqrt(np.mean(e * e)))
+    assert np.all(np.isfinite(got)), what
+    assert mx <= MAX_ABS and rm <= RMSE, f"{what}: max-abs {mx:.3e} rmse {rm:.3e}"
+    return mx, rm
+
+
+# ------------------------------------------------------------------ whole images vs the oracle
+
+SMALL = {
+    "cfg0": (256, 256),          # cfg0 at its full size
+    "cfg1": (300, 347),
+    "cfg2": (333, 361),          # r = 48: 3 strips (TW = 160) + ragged tail, 2 bands
+    "cfg3": (211, 333),
+    "cfg4": (419, 430),          # r = 192, Tukey, 24 terms: 3 passes, 4 strips
+}
+
+
+@pytest.mark.parametrize("cfg", sorted(SMALL))
+def test_config_small_full_image(gpu, cfg):
+    pkg, torch = gpu
+    spec = CONFIGS[cfg]
+    H, W = SMALL[cfg]
+    img = config_input(spec, H=H, W=W)
+    gp, op = make_plans(pkg, config_params(spec), img.dtype)
+    got = run_gpu(pkg, torch, gp, img)
+    ref = bf.bf_box(img, op)
+    assert_parity(got, ref, spec.intensity_max, cfg)
+
+
+def sample_pixels(H, W, r, n, seed):
+    rng = np.random.default_rng(seed)
+    pts = {(0, 0), (0, W - 1), (H - 1, 0), (H - 1, W - 1), (H // 2, W // 2), (min(r, H - 1), min(r, W - 1)),
+           (H - 1 - min(r, H - 1), W // 3)}
+    while len(pts) < n:
+        pts.add((int(rng.integers(0, H)), int(rng.integers(0, W))))
+    return sorted(pts)
+
+
+@pytest.mark.parametrize("cfg,n", [("cfg1", 48), ("cfg2", 48), ("cfg3", 32), ("cfg4", 24)])
+def test_config_full_size_sampled(gpu, cfg, n):
+    """Full BASELINE size, launched exactly as bench.py launches it; the oracle evaluates the
+    same approximation directly at sampled pixels (pin P1 ties it to the box evaluation)."""
+    pkg, torch = gpu
+    spec = CONFIGS[cfg]
+    img = config_input(spec)
+    gp, op = make_plans(pkg, config_params(spec), img.dtype)
+    got = run_gpu(pkg, torch, gp, img)
+    pts = sample_pixels(spec.H, spec.W, spec.radius, n, seed=7)
+    ref, _, _ = bf.bf_direct(img, op, pixels=pts)
+    vals = np.array([got[y, x] for (y, x) in pts])
+    assert_parity(vals, ref, spec.intensity_max, cfg)
+    # properties that hold at any size: finite, within [0, D] up to the approximation slack
+    assert np.all(np.isfinite(got))
+    D = spec.intensity_max
+    assert got.min() > -0.1 * D and got.max() < 1.1 * D
+
+
+def test_cfg3_batched_frames_match_single_calls(gpu):
+    pkg, torch = gpu
+    spec = CONFIGS["cfg3"]
+    H, W = 120, 207
+    frames = np.stack([config_input(spec, frame=f, H=H, W=W) for f in range(3)])
+    gp, op = make_plans(pkg, config_params(spec), frames.dtype)
+    t = torch.from_numpy(frames).cuda()
+    outb = pkg.bilateral_filter(gp, t).cpu().numpy()
+    for f in range(3):
+        single = run_gpu(pkg, torch, gp, frames[f])
+        assert np.array_equal(outb[f], single.astype(np.float32))
+        assert_parity(single, bf.bf_box(frames[f], op), 255.0, f"frame {f}")
+
+
+# ------------------------------------------------------------------ edge cases
+
+@pytest.mark.parametrize("H,W", [(1, 1), (1, 57), (61, 1), (5, 7), (7, 300), (300, 6), (17, 33)])
+def test_degenerate_shapes(gpu, H, W):
+    pkg, torch = gpu
+    spec = CONFIGS["cfg1"]
+    img = config_input(spec, H=max(H, 2), W=max(W, 2))[:H, :W].copy()
+    gp, op = make_plans(pkg, config_params(spec), img.dtype)
+    assert_parity(run_gpu(pkg, torch, gp, img), bf.bf_box(img, op), 255.0, f"{H}x{W}")
+
+
+def test_constant_image(gpu):
+    pkg, torch = gpu
+    img = np.full((70, 90), 0.625, dtype=np.float32)
+    gp, op = make_plans(pkg, config_params(CONFIGS["cfg2"]), img.dtype, radius=20)
+    got = run_gpu(pkg, torch, gp, img)
+    assert np.max(np.abs(got - 0.625)) * 255 <= MAX_ABS
+
+
+def test_radius_zero_identity(gpu):
+    pkg, torch = gpu
+    img = config_input(CONFIGS["cfg0"], H=40, W=50)
+    gp, op = make_plans(pkg, config_params(CONFIGS["cfg0"]), img.dtype, radius=0)
+    assert_parity(run_gpu(pkg, torch, gp, img), img.astype(np.float64), 255.0, "r=0")
+
+
+def test_infinite_sigma_r(gpu):
+    pkg, torch = gpu
+    img = config_input(CONFIGS["cfg1"], H=64, W=80)
+    gp, op = make_plans(pkg, config_params(CONFIGS["cfg1"]), img.dtype, sigma_r=math.inf)
+    assert gp.info()["k"] == [0]
+    assert_parity(run_gpu(pkg, torch, gp, img), bf.bf_box(img, op), 255.0, "sigma_r=inf")
+
+
+def test_u8_and_f32_inputs_agree(gpu):
+    pkg, torch = gpu
+    spec = CONFIGS["cfg0"]
+    img8 = config_input(spec, H=90, W=110)
+    g8, op = make_plans(pkg, config_params(spec), np.uint8)
+    g32, _ = make_plans(pkg, config_params(spec), np.float32)
+    o8 = run_gpu(pkg, torch, g8, img8)
+    o32 = run_gpu(pkg, torch, g32, img8.astype(np.float32))
+    ref = bf.bf_box(img8, op)
+    assert_parity(o8, ref, 255.0, "u8")
+    assert_parity(o32, ref, 255.0, "f32")
+
+
+def test_deterministic(gpu):
+    pkg, torch = gpu
+    spec = CONFIGS["cfg2"]
+    img = config_input(spec, H=200, W=230)
+    gp, _ = make_plans(pkg, config_params(spec), img.dtype)
+    a = run_gpu(pkg, torch, gp, img)
+    b = run_gpu(pkg, torch, gp, img)
+    assert np.array_equal(a, b)
+
+
+def test_rank2_plan_is_rejected_loudly(gpu):
+    pkg, torch = gpu
+    gp, _ = make_plans(pkg, config_params(CONFIGS["cfg0"]), np.float32, n_spatial=5)
+    img = torch.zeros((32, 32), dtype=torch.float32, device="cuda")
+    with pytest.raises(pkg.BFError):
+        pkg.bilateral_filter(gp, img)
