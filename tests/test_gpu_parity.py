@@ -130,7 +130,7 @@ def test_degenerate_shapes(gpu, H, W):
 def test_constant_image(gpu):
     pkg, torch = gpu
     img = np.full((70, 90), 0.625, dtype=np.float32)
-    gp, op = make_plans(pkg, config_params(CONFIGS["cfg2"]), img.dtype, radius=20)
+    gp, op = make_plans(pkg, config_params(CONFIGS["cfg2"]), img.dtype, radius=20, sigma_s=6.0)
     got = run_gpu(pkg, torch, gp, img)
     assert np.max(np.abs(got - 0.625)) * 255 <= MAX_ABS
 
