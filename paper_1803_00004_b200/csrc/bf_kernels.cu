@@ -1,69 +1,79 @@
-// Fused sm_100a kernel of the joint-acceleration bilateral filter (bf_apply).
+// Fused sm_100a kernel of the joint-acceleration bilateral filter (bf_apply), version 6.
 //
-// Evaluates eq:numerator_2D_box_N_terms with T = D (Q1): for every selected
-// cosine term k the four channels g^c_k, g^s_k, G^c_k = I g^c_k, G^s_k = I g^s_k are
-// generated in registers, box-filtered with the separable Haar-box kernel
-// K~_s(u, v) = fx(u) fy(v) (eq:2D_box_N_terms_s, Appendix A), and recombined with
-// a_k g^c_k(x), a_k g^s_k(x); out = num / den (eq:BF).
+// Evaluates eq:numerator_2D_box_N_terms with T = D (Q1): for every selected cosine
+// term k the four channels g^c_k = cos(w_k I), g^s_k = sin(w_k I), G^c_k = I g^c_k,
+// G^s_k = I g^s_k are generated in registers, box-filtered with the separable Haar-box
+// kernel K~_s(u, v) = fx(u) fy(v) (eq:2D_box_N_terms_s, Appendix A), and recombined
+// with a_k g^c_k(x), a_k g^s_k(x) (Q17); out = num / den (eq:BF).
 //
-// Layout of one CTA: a vertical strip of TW output columns plus the horizontal halo
-// (NTC = blockDim.x extended columns, one thread per column) and a band of TH output rows.
-// Per output row:
-//   V  each thread slides the vertical box sums of all channels of its column down one row:
-//      channels at the entering / leaving rows of every box are regenerated from I (rotation
-//      recurrence from an accurately reduced base angle) and quantised to 22-bit fixed point
-//      with one FFMA (x*s + 1.5*2^23), so the sliding sums are EXACT int32 arithmetic with no
-//      drift; U = sum_b wy_b S_b is re-quantised and written to shared memory.
-//   H  walker threads (channel, segment) slide the horizontal box sums of U along the row in
-//      exact int32 arithmetic and write F = sum_b wx_b H_b (fp32) to shared memory.
-//   C  one thread per output pixel regenerates its weights a_k cos/sin(pi k I(x)/D) and
-//      accumulates num / den (fp32 products, fp64 accumulation per group of k), then divides.
-// Nothing but the input image and the output image touches HBM.
+// A CTA owns a vertical strip (NT extended columns = TW output columns plus the horizontal
+// halo, one thread per extended column) and a band of TH output rows. Per output row y it runs
+// two barrier-separated intervals:
+//   A  V(y): every thread slides the vertical box sums of all channels of its column down one
+//      row. The box weight wy_b is folded into the per-tap quantisation scale, so the state is
+//      ONE exact int32 per channel (U = sum_b sum_v rint(wy_b X 2^q)); taps are regenerated
+//      from I by a Chebyshev recurrence (cos (k+1)t = 2 cos t cos kt - cos (k-1)t) from a
+//      polynomial (f32) or LUT (u8) base angle and quantised with one FFMA2 per tap pair
+//      (x*s + 1.5*2^23 has the integer rint(x*s) in its low mantissa bits). U' = U >> ush goes
+//      to shared memory.
+//      C(y-1): one thread per output pixel computes the combine weights a_k cos/sin(k pi I(x)/D)
+//      in fp64 (Chebyshev again), rounds them to integers with the fp64 magic-number trick,
+//      accumulates num / den exactly in int64 from the F row of y-1 and writes D*num/den (or
+//      I(x) if den <= 0, Q18).
+//   B  H(y): walkers slide the exact int32 horizontal box sums of U' along the row. Lanes of a
+//      warp are 32 channels at the SAME x (conflict-free shared-memory access); each writes
+//      F = sum_b ax_b H_b (exact int64, narrowed to int32) to shared memory.
+// Nothing but the input image and the output image touches HBM (plus an int64 num/den
+// workspace when the terms do not fit one pass).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
-#include <vector>
 
 #include "bf_internal.h"
 
 namespace {
 
-constexpr int QMAX = (1 << 22) - 1;       // |quantised channel value| <= QMAX
-constexpr float MAGIC = 12582912.0f;      // 1.5 * 2^23: fma(x, s, MAGIC) has bits 0x4B400000 + rint(x*s)
-constexpr int MAXB = 4;                   // boxes per axis of the separable spatial factor
-constexpr int ABITS = 27;                 // integer horizontal box weights
-constexpr int WBITS = 29;                 // integer combine weights
+constexpr float MAGIC = 12582912.0f;              // 1.5 * 2^23
+constexpr int MAGIC_BITS = 0x4B400000;            // bit pattern of MAGIC
+constexpr double MAGIC64 = 6755399441055744.0;    // 1.5 * 2^52: low word of fma(x, s, MAGIC64) = rint(x*s)
+constexpr int QBITS_MAX = 22;                     // channel quantisation (the FFMA trick's range)
+constexpr int ABITS = 27;                         // horizontal integer box weights
+constexpr int MAXB = 4;                           // boxes per axis
 
 struct KParams {
   int H, W;
-  int nk;                   // cosine terms handled by this launch
-  int kstep[BF_MAX_TERMS];  // rotation steps from the previous term (first: from k0)
-  float a[BF_MAX_TERMS];    // a_k
-  int k0;                   // k of the term before the first one of this launch (0 for pass 0)
+  long long frame_elems;
+  int TW, TH, rlo_x;
   int nbx, nby;
-  int lox[MAXB], hix[MAXB], loy[MAXB], hiy[MAXB];
-  int ax[MAXB];             // horizontal box weights as integers: round(wx_b / max|wx| * 2^27)
-  int fshift;               // F32 = (sum_b ax_b H_b) >> fshift fits in int32
-  int ay[MAXB];             // vertical box weights as integers: round(wy_b / max|wy| * 2^27)
-  float qD;                 // QMAX / D (scale of the I cos / I sin channels; cos / sin use QMAX)
-  int vlo, vhi;             // union of the vertical boxes (rows v with some box containing v)
-  int rlo_x;                // -min lox (left halo)
-  int ushift;               // U' = (sum_b ay_b S_b) >> ushift keeps the horizontal sums in int32
-  int TW, TH;               // output strip width / band height
-  float invD_hi, invD_lo;   // 1/D as a float-float pair
-  float D;
-  float aw[BF_MAX_TERMS];   // a_k * 2^WBITS: combine weights quantised as rint(aw * cos/sin)
-  int pass;                 // 0 = only pass; 1 = first; 2 = middle; 3 = last
-  long long frame_elems;    // H * W (batched frames)
+  int vlo[MAXB], vhi[MAXB];   // vertical boxes: row offsets (inclusive)
+  float qs[MAXB];             // their quantisation scales wy_b / max|wy| * 2^q (cos / sin channels)
+  float qsD[MAXB];            // qs_b / D (I cos / I sin channels)
+  int vmin, vmax;             // union of the vertical boxes
+  int urnd, ush;              // U' = (U + urnd) >> ush; urnd is folded into the initial state
+  int hlo[MAXB], hhi[MAXB];   // horizontal boxes: column offsets (inclusive)
+  int ax[MAXB];               // their integer weights round(wx_b / max|wx| * 2^27)
+  int fsh;                    // F = (sum_b ax_b H_b + frnd) >> fsh fits int32
+  long long frnd;
+  int nk;                     // terms of this pass
+  int kstep[BF_MAX_TERMS];    // Chebyshev steps before term i (term 0: from k = 0)
+  double aw[BF_MAX_TERMS];    // a_k * 2^wbits
+  float invD_hi, invD_lo;     // 1/D as a float-float pair
+  double invD, D;
+  int pass;                   // 0 = only pass; 1 = first; 2 = middle; 3 = last
+  int ngrp, nseg, seglen;     // walkers: 32-channel groups x row segments
+  int f_off, l_off;           // shared-memory carve-up: U' [4 nk][NT+1] int, F [TW][4 MAXK + 4] int,
+                              // LUTs (u8) float2[256] + double2[256]
 };
 
 typedef unsigned long long u64;
 
-// ---- packed fp32x2 helpers (sm_100a FFMA2 / FMUL2: two lanes of work per issue slot)
+// ---- packed fp32x2 helpers (sm_100a FFMA2: two lanes of work per issue slot)
 __device__ __forceinline__ u64 pk(float a, float b) {
   u64 r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
@@ -74,109 +84,138 @@ __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
-__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
-  u64 r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-// (lo - hi) of the integer bit patterns of a packed pair of quantised values
+// q(lo) - q(hi) of a packed pair of quantised values (the MAGIC bias cancels)
 __device__ __forceinline__ int diff_bits(u64 v) {
   int a, b;
   asm("mov.b64 {%0, %1}, %2;" : "=r"(a), "=r"(b) : "l"(v));
   return a - b;
 }
+__device__ __forceinline__ int quant(float x, float s) { return __float_as_int(fmaf(x, s, MAGIC)) - MAGIC_BITS; }
 
 __device__ __forceinline__ float load_pixel(const void* in, bool u8, long long idx) {
   if (u8) return (float)__ldg(reinterpret_cast<const unsigned char*>(in) + idx);
   return __ldg(reinterpret_cast<const float*>(in) + idx);
 }
 
-// cos(pi I / D), sin(pi I / D) with I/D carried as a float-float pair and a first-order
-// correction for its low part (the naive fp32 phase fails the tolerance).
-__device__ __forceinline__ void base_angle(float I, const KParams& P, float& c1, float& s1) {
-  float t = I * P.invD_hi;
-  float e = fmaf(I, P.invD_hi, -t) + I * P.invD_lo;
-  float s, c;
-  sincospif(t, &s, &c);
-  float pe = 3.14159265358979323846f * e;
-  c1 = fmaf(-s, pe, c);
-  s1 = fmaf(c, pe, s);
+// cos(pi I / D), sin(pi I / D) in fp32 for I in [0, D]: t' = I/D - 1/2 (float-float 1/D),
+// sin(pi t') = t' P(t'^2), cos(pi t') = Q(t'^2) (least-squares minimax fits, |err| <= 2e-7,
+// tools/numerics_v6.py), cos(pi t) = -sin(pi t'), sin(pi t) = cos(pi t').
+__device__ __forceinline__ void base_angle_f32(float I, const KParams& P, float& c1, float& s1) {
+  float t = fmaf(I, P.invD_hi, -0.5f);
+  t = fmaf(I, P.invD_lo, t);
+  const float z = t * t;
+  float p = -7.022163365e-03f;
+  p = fmaf(p, z, 8.204647899e-02f);
+  p = fmaf(p, z, -5.992513299e-01f);
+  p = fmaf(p, z, 2.550163269e+00f);
+  p = fmaf(p, z, -5.167712688e+00f);
+  p = fmaf(p, z, 3.141592741e+00f);
+  float q = -1.004332444e-04f;
+  q = fmaf(q, z, 1.927883714e-03f);
+  q = fmaf(q, z, -2.580653690e-02f);
+  q = fmaf(q, z, 2.353305817e-01f);
+  q = fmaf(q, z, -1.335262775e+00f);
+  q = fmaf(q, z, 4.058712006e+00f);
+  q = fmaf(q, z, -4.934802055e+00f);
+  q = fmaf(q, z, 1.0f);
+  c1 = -p * t;
+  s1 = q;
 }
 
-__device__ __forceinline__ void rotate(float& c, float& s, float c1, float s1) {
-  float cn = fmaf(c, c1, -s * s1);
-  float sn = fmaf(s, c1, c * s1);
+// The same angle in fp64 for the combine weights: Taylor series of sin(pi t') / t' and
+// cos(pi t') to degree 21 / 22 (truncation < 2e-18 on |t'| <= 1/2), Horner in DFMA.
+__constant__ double kSinPi64[11] = {3.14159265358979312e+00, -5.16771278004996937e+00, 2.55016403987734508e+00,
+                                     -5.99264529320791883e-01, 8.21458866111281910e-02, -7.37043094571434784e-03,
+                                     4.66302805767612337e-04, -2.19153534478302037e-05, 7.95205400147550838e-07,
+                                     -2.29484289972698565e-08, 5.39266466260812482e-10};
+__constant__ double kCosPi64[12] = {1.0, -4.93480220054467900e+00, 4.05871212641676760e+00, -1.33526276885458928e+00,
+                                    2.35330630358893123e-01, -2.58068913900140508e-02, 1.92957430940392206e-03,
+                                    -1.04638104924845650e-04, 4.30306958703294391e-06, -1.38789524622137608e-07,
+                                    3.60473079746249822e-09, -7.70070713060134610e-11};
+
+// The same angle in fp64 for the combine weights: Taylor series of sin(pi t') / t' and
+// cos(pi t') to degree 21 / 22 (truncation < 2e-18 on |t'| <= 1/2), Horner in DFMA with the
+// coefficients as constant-bank operands.
+__device__ __forceinline__ void base_angle_f64(float I, double invD, double& c1, double& s1) {
+  const double t = fma((double)I, invD, -0.5);
+  const double z = t * t;
+  double p = kSinPi64[10];
+#pragma unroll
+  for (int i = 9; i >= 0; --i) p = fma(p, z, kSinPi64[i]);
+  double q = kCosPi64[11];
+#pragma unroll
+  for (int i = 10; i >= 0; --i) q = fma(q, z, kCosPi64[i]);
+  c1 = -p * t;
+  s1 = q;
+}
+
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// Rotation recurrence (c, s)_{k+1} = (c c1 - s s1, s c1 + c s1) on a packed pair of taps:
+// 2 FMUL2 + 2 FFMA2 per step, no register shuffling. rot1() is the bit-identical scalar form.
+struct Rot2 {
+  u64 C, S, C1, S1, NS1;
+  __device__ __forceinline__ void init(float ca, float sa, float cb, float sb) {
+    C = pk(1.f, 1.f);
+    S = pk(0.f, 0.f);
+    C1 = pk(ca, cb);
+    S1 = pk(sa, sb);
+    NS1 = pk(-sa, -sb);
+  }
+  __device__ __forceinline__ void step() {
+    const u64 Cn = fma2(S, NS1, mul2(C, C1));
+    const u64 Sn = fma2(C, S1, mul2(S, C1));
+    C = Cn;
+    S = Sn;
+  }
+};
+__device__ __forceinline__ void rot1(float& c, float& s, float c1, float s1) {
+  const float cn = fmaf(s, -s1, c * c1);
+  const float sn = fmaf(c, s1, s * c1);
   c = cn;
   s = sn;
 }
 
-template <bool U8>
-__device__ __forceinline__ void tap_base(const void* in, const KParams& P, const float2* lut, int row, int col,
-                                         long long fbase, float& c1, float& s1, float& I, bool& valid) {
-  valid = (row >= 0) & (row < P.H) & (col >= 0) & (col < P.W);
-  I = 0.f;
-  if (valid) I = load_pixel(in, U8, fbase + (long long)row * P.W + col);
-  if (U8) {
-    float2 v = lut[(int)I];
-    c1 = v.x;
-    s1 = v.y;
-  } else {
-    base_angle(I, P, c1, s1);
+struct Cheb64 {
+  double c, s, cp, sp, c2;
+  __device__ __forceinline__ void init(double c1, double s1) {
+    c = 1.0;
+    s = 0.0;
+    cp = c1;
+    sp = -s1;
+    c2 = c1 + c1;
   }
-}
-
-// Channels of one cosine term for a packed pair of taps (lo half = entering row, hi half =
-// leaving row): cos, sin, I cos, I sin quantised with FFMA against MAGIC; the state gains
-// q(enter) - q(leave) exactly (int32 arithmetic on the bit patterns, the bias cancels).
-__device__ __forceinline__ void accumulate_pair(int* St, u64 C, u64 S, u64 SC1, u64 SCD) {
-  const u64 MM = pk(MAGIC, MAGIC);
-  St[0] += diff_bits(fma2(C, SC1, MM));
-  St[1] += diff_bits(fma2(S, SC1, MM));
-  St[2] += diff_bits(fma2(C, SCD, MM));
-  St[3] += diff_bits(fma2(S, SCD, MM));
-}
-
-__device__ __forceinline__ void rotate2(u64& C, u64& S, u64 C1, u64 S1, u64 NS1) {
-  u64 Cn = fma2(S, NS1, mul2(C, C1));
-  u64 Sn = fma2(C, S1, mul2(S, C1));
-  C = Cn;
-  S = Sn;
-}
-
-// sum of U[a..b] (inclusive), 16-byte vector loads where aligned
-__device__ __forceinline__ int range_sum(const int* U, int a, int b) {
-  int s = 0, j = a;
-  for (; j <= b && (reinterpret_cast<uintptr_t>(U + j) & 15) != 0; ++j) s += U[j];
-  for (; j + 3 <= b; j += 4) {
-    const int4 v = *reinterpret_cast<const int4*>(U + j);
-    s += v.x + v.y + v.z + v.w;
+  __device__ __forceinline__ void step() {
+    const double cn = fma(c2, c, -cp);
+    const double sn = fma(c2, s, -sp);
+    cp = c;
+    sp = s;
+    c = cn;
+    s = sn;
   }
-  for (; j <= b; ++j) s += U[j];
-  return s;
-}
+};
 
-// F = (sum_b ax_b H_b) >> fshift: exact int64 weighted box sum narrowed to int32.
-template <int NB>
-__device__ __forceinline__ int combine_boxes(const int* Hs, const KParams& P) {
-  long long f = (long long)P.ax[0] * Hs[0];
-#pragma unroll
-  for (int b = 1; b < NB; ++b)
-    if (b < P.nbx) f += (long long)P.ax[b] * Hs[b];
-  return (int)(f >> P.fshift);
-}
 
-template <int MAXK, bool U8, int NT, bool CONSEC, int NB>
-__global__ void __launch_bounds__(NT, 1) bf_strip_kernel(const KParams P, const void* __restrict__ in,
-                                                         float* __restrict__ out, longlong2* __restrict__ ws) {
-  constexpr int C = 4 * MAXK;
-  constexpr int R = 2;                                                // output rows per iteration
+// resident CTAs per SM the register budget is sized for
+template <int MAXK, int NT>
+struct Occ {
+  static constexpr int value = NT > 256 ? 1 : 2;
+};
+
+// FULL: nk == MAXK (no per-term runtime checks). CONSEC: the selected k are consecutive.
+template <int MAXK, int NB, bool U8, int NT, bool CONSEC, bool FULL>
+__global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
+    bf_band_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out,
+                   longlong2* __restrict__ ws) {
+  constexpr int UP = NT + 1;   // channel-row pitch (== 1 mod 32: lanes = channels are conflict-free)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int UPITCH = NT + 1;
-  const int FPITCH = P.TW + 1;
-  const int nch = 4 * P.nk;                                           // channels of this launch
-  float2* lut = reinterpret_cast<float2*>(smem_raw);                  // [256] (u8 only)
-  int* Ubuf = reinterpret_cast<int*>(lut + 256);                      // [R][nch][UPITCH]
-  int* Fbuf = Ubuf + R * nch * UPITCH;                                // [R][nch][FPITCH]
+  int* Ubuf = reinterpret_cast<int*>(smem_raw);                               // [4 nk][UP]
+  float2* lut = reinterpret_cast<float2*>(smem_raw + P.l_off);                // [256]
+  double2* lut64 = reinterpret_cast<double2*>(lut + 256);                     // [256]
 
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * P.TW;
@@ -186,69 +225,73 @@ __global__ void __launch_bounds__(NT, 1) bf_strip_kernel(const KParams P, const 
   const bool colok = (col >= 0) & (col < P.W);
   const int TWv = min(P.TW, P.W - x0);
   const int yend = min(y0 + P.TH, P.H);
+  const int nk = P.nk;
 
   if (U8) {
     for (int i = tid; i < 256; i += NT) {
       double s, c;
-      sincospi((double)i / (double)P.D, &s, &c);
+      sincospi((double)i * P.invD, &s, &c);
       lut[i] = make_float2((float)c, (float)s);
+      lut64[i] = make_double2(c, s);
     }
     __syncthreads();
   }
 
-  // ---- vertical state at row y0 - 1: exact int32 box sums S_b of every channel, one per box
-  //      of fy (each channel value quantised ONCE at full 22-bit scale; folding the box weights
-  //      into the quantisation loses the tolerance).
-  int S[NB][C];
+  // ------------------------------------------------------------ vertical state at row y0 - 1
+  int U[4 * MAXK];
 #pragma unroll
-  for (int b = 0; b < NB; ++b)
+  for (int ch = 0; ch < 4 * MAXK; ++ch) U[ch] = P.urnd;
+  for (int v = P.vmin; v <= P.vmax; ++v) {
+    const int row = y0 - 1 + v;
+    const bool ok = colok && row >= 0 && row < P.H;
+    const float I = ok ? load_pixel(in, U8, fbase + (long long)row * P.W + col) : 0.f;
+    float c1, s1;
+    if (U8) {
+      const float2 t = lut[(int)I];
+      c1 = t.x;
+      s1 = t.y;
+    } else {
+      base_angle_f32(I, P, c1, s1);
+    }
+    float sc = 0.f, scI = 0.f;   // sum of the scales of the boxes that contain v (nested or not)
+    float scb[NB], scIb[NB];
 #pragma unroll
-    for (int ch = 0; ch < C; ++ch) S[b][ch] = 0;
-
-  for (int v = P.vlo; v <= P.vhi; ++v) {
-    float c1, s1, I;
-    bool valid;
-    tap_base<U8>(in, P, lut, y0 - 1 + v, col, fbase, c1, s1, I, valid);
-    const float sc1 = valid ? (float)QMAX : 0.f, scD = valid ? P.qD * I : 0.f;
-    bool inb[NB];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) inb[b] = (b < P.nby) && v >= P.loy[b] && v <= P.hiy[b];
-    float c = 1.f, s = 0.f;
-    for (int j = 0; j < P.k0; ++j) rotate(c, s, c1, s1);
+    for (int b = 0; b < NB; ++b) {
+      const bool in_b = ok && (b < P.nby) && v >= P.vlo[b] && v <= P.vhi[b];
+      scb[b] = in_b ? P.qs[b] : 0.f;
+      scIb[b] = in_b ? P.qsD[b] * I : 0.f;
+    }
+    (void)sc;
+    (void)scI;
+    float gc = 1.f, gs = 0.f;
+    for (int j = 0; j < P.kstep[0]; ++j) rot1(gc, gs, c1, s1);
 #pragma unroll
     for (int i = 0; i < MAXK; ++i) {
-      if (i < P.nk) {
-        if (CONSEC) {
-          if (i > 0) rotate(c, s, c1, s1);
-        } else {
-          for (int j = 0; j < P.kstep[i]; ++j) rotate(c, s, c1, s1);
+      if (FULL || i < nk) {
+        if (i > 0) {
+          if (CONSEC) rot1(gc, gs, c1, s1);
+          else
+            for (int j = 0; j < P.kstep[i]; ++j) rot1(gc, gs, c1, s1);
         }
-        const int q0 = __float_as_int(fmaf(c, sc1, MAGIC)) - 0x4B400000;
-        const int q1 = __float_as_int(fmaf(s, sc1, MAGIC)) - 0x4B400000;
-        const int q2 = __float_as_int(fmaf(c, scD, MAGIC)) - 0x4B400000;
-        const int q3 = __float_as_int(fmaf(s, scD, MAGIC)) - 0x4B400000;
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
-          if (inb[b]) {
-            S[b][4 * i] += q0;
-            S[b][4 * i + 1] += q1;
-            S[b][4 * i + 2] += q2;
-            S[b][4 * i + 3] += q3;
-          }
+          U[4 * i + 0] += quant(gc, scb[b]);
+          U[4 * i + 1] += quant(gs, scb[b]);
+          U[4 * i + 2] += quant(gc, scIb[b]);
+          U[4 * i + 3] += quant(gs, scIb[b]);
         }
       }
     }
   }
 
-  // tap rows of the iteration whose first output row is ya, per box b:
-  //   j=0 enter(ya) = ya + hi, j=1 leave(ya) = ya - 1 + lo, j=2 enter(ya+1), j=3 leave(ya+1)
-  float Ipre[NB][4];
-  auto load_taps = [&](int ya) {
+  // tap rows of output row y, box b: enter y + vhi_b, leave y + vlo_b - 1
+  float Ipre[NB][2];
+  auto load_taps = [&](int y) {
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int row = ya + ((j & 2) ? 1 : 0) + ((j & 1) ? (P.loy[b] - 1) : P.hiy[b]);
+      for (int j = 0; j < 2; ++j) {
+        const int row = y + (j ? (P.vlo[b] - 1) : P.vhi[b]);
         const bool ok = (b < P.nby) && colok && row >= 0 && row < P.H;
         Ipre[b][j] = ok ? load_pixel(in, U8, fbase + (long long)row * P.W + col) : 0.f;
       }
@@ -256,198 +299,98 @@ __global__ void __launch_bounds__(NT, 1) bf_strip_kernel(const KParams P, const 
   };
   load_taps(y0);
 
-  // walker assignment for the H phase: (row r, channel, segment)
-  const int nwalk = R * nch;
-  const int nseg = max(1, NT / max(nwalk, 1));
-  const int seglen = (TWv + nseg - 1) / nseg;
-  const int wr = tid / (nch * nseg);
-  const int wch = (tid / nseg) % max(nch, 1);
-  const int wseg = tid % nseg;
-  const long long uround = P.ushift > 0 ? (1LL << (P.ushift - 1)) : 0;
+  // walker of this thread (interval B): lane = channel slot, warp = (slot group, segment)
+  const int wgrp = (tid >> 5) % P.ngrp;
+  const int wseg = (tid >> 5) / P.ngrp;
+  const int wslot = wgrp * 32 + (tid & 31);
+  const bool wact = (wslot < 4 * nk) && (wseg < P.nseg);
+  constexpr int FPX = 4 * MAXK + 4;   // F pitch per output column (4 * odd: conflict-free int4 reads)
+  int* Fbuf = reinterpret_cast<int*>(smem_raw + P.f_off);   // [TW][FPX]: F of output column x, channel slot
+  float Ic = 0.f;   // I(y - 1, x0 + tid) for the combine of row y - 1 (threads < TWv)
 
-  for (int ya = y0; ya < yend; ya += R) {
-    // ---------------------------------------------------------------- V: slide two rows
-    {
-      u64 C1A[NB], S1A[NB], NS1A[NB], SC1A[NB], SCDA[NB], CA[NB], SA[NB];
-      u64 C1B[NB], S1B[NB], NS1B[NB], SC1B[NB], SCDB[NB], CB[NB], SB[NB];
+  for (int y = y0; y <= yend; ++y) {
+    // ============================================================ interval A
+    if (y < yend) {
+      // ---------------------------------------------------------- V(y): slide one row
+      u64 QS[NB], QI[NB];
+      Rot2 g2[NB];
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
-        float c1[4], s1[4], sc1[4], scD[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int row = ya + ((j & 2) ? 1 : 0) + ((j & 1) ? (P.loy[b] - 1) : P.hiy[b]);
-          const bool ok = (b < P.nby) && colok && row >= 0 && row < P.H;
-          const float I = Ipre[b][j];
-          if (U8) {
-            const float2 t = lut[(int)I];
-            c1[j] = t.x;
-            s1[j] = t.y;
-          } else {
-            base_angle(I, P, c1[j], s1[j]);
-          }
-          sc1[j] = ok ? (float)QMAX : 0.f;
-          scD[j] = ok ? P.qD * I : 0.f;
-        }
-        C1A[b] = pk(c1[0], c1[1]);
-        S1A[b] = pk(s1[0], s1[1]);
-        NS1A[b] = pk(-s1[0], -s1[1]);
-        SC1A[b] = pk(sc1[0], sc1[1]);
-        SCDA[b] = pk(scD[0], scD[1]);
-        C1B[b] = pk(c1[2], c1[3]);
-        S1B[b] = pk(s1[2], s1[3]);
-        NS1B[b] = pk(-s1[2], -s1[3]);
-        SC1B[b] = pk(sc1[2], sc1[3]);
-        SCDB[b] = pk(scD[2], scD[3]);
-        if (CONSEC) {
-          CA[b] = CB[b] = pk(1.f, 1.f);
-          SA[b] = SB[b] = pk(0.f, 0.f);
+        float ce, se, cl, sl;
+        const float Ie = Ipre[b][0], Il = Ipre[b][1];
+        if (U8) {
+          const float2 te = lut[(int)Ie], tl = lut[(int)Il];
+          ce = te.x; se = te.y; cl = tl.x; sl = tl.y;
         } else {
-          float cc[4] = {1.f, 1.f, 1.f, 1.f}, ss[4] = {0.f, 0.f, 0.f, 0.f};
-          for (int j = 0; j < P.k0; ++j)
-#pragma unroll
-            for (int t = 0; t < 4; ++t) rotate(cc[t], ss[t], c1[t], s1[t]);
-          CA[b] = pk(cc[0], cc[1]);
-          SA[b] = pk(ss[0], ss[1]);
-          CB[b] = pk(cc[2], cc[3]);
-          SB[b] = pk(ss[2], ss[3]);
+          base_angle_f32(Ie, P, ce, se);
+          base_angle_f32(Il, P, cl, sl);
         }
+        const int re = y + P.vhi[b], rl = y + P.vlo[b] - 1;
+        const bool oke = (b < P.nby) && colok && re >= 0 && re < P.H;
+        const bool okl = (b < P.nby) && colok && rl >= 0 && rl < P.H;
+        QS[b] = pk(oke ? P.qs[b] : 0.f, okl ? P.qs[b] : 0.f);
+        QI[b] = pk(oke ? P.qsD[b] * Ie : 0.f, okl ? P.qsD[b] * Il : 0.f);
+        g2[b].init(ce, se, cl, sl);
+        for (int j = 0; j < P.kstep[0]; ++j) g2[b].step();
       }
-      if (ya + R < yend) load_taps(ya + R);   // prefetch: completes during the H and C phases
+      if (y + 1 < yend) load_taps(y + 1);   // prefetch: lands during this row's work
       const u64 MM = pk(MAGIC, MAGIC);
 #pragma unroll
       for (int i = 0; i < MAXK; ++i) {
-        if (i < P.nk) {
+        if (FULL || i < nk) {
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
-            if (CONSEC) {
-              if (i > 0) {
-                rotate2(CA[b], SA[b], C1A[b], S1A[b], NS1A[b]);
-                rotate2(CB[b], SB[b], C1B[b], S1B[b], NS1B[b]);
-              }
-            } else {
-              for (int j = 0; j < P.kstep[i]; ++j) {
-                rotate2(CA[b], SA[b], C1A[b], S1A[b], NS1A[b]);
-                rotate2(CB[b], SB[b], C1B[b], S1B[b], NS1B[b]);
-              }
+            if (i > 0) {
+              if (CONSEC) g2[b].step();
+              else
+                for (int j = 0; j < P.kstep[i]; ++j) g2[b].step();
             }
-          }
-          int da[NB][4], db[NB][4];
-#pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            da[b][0] = diff_bits(fma2(CA[b], SC1A[b], MM));
-            da[b][1] = diff_bits(fma2(SA[b], SC1A[b], MM));
-            da[b][2] = diff_bits(fma2(CA[b], SCDA[b], MM));
-            da[b][3] = diff_bits(fma2(SA[b], SCDA[b], MM));
-            db[b][0] = diff_bits(fma2(CB[b], SC1B[b], MM));
-            db[b][1] = diff_bits(fma2(SB[b], SC1B[b], MM));
-            db[b][2] = diff_bits(fma2(CB[b], SCDB[b], MM));
-            db[b][3] = diff_bits(fma2(SB[b], SCDB[b], MM));
+            const u64 C = g2[b].C, Sn = g2[b].S;
+            U[4 * i + 0] += diff_bits(fma2(C, QS[b], MM));
+            U[4 * i + 1] += diff_bits(fma2(Sn, QS[b], MM));
+            U[4 * i + 2] += diff_bits(fma2(C, QI[b], MM));
+            U[4 * i + 3] += diff_bits(fma2(Sn, QI[b], MM));
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int ch = 4 * i + j;
-            long long ua = uround, ub = uround;
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-              if (b < P.nby) {
-                S[b][ch] += da[b][j];
-                ua += (long long)P.ay[b] * S[b][ch];
-                S[b][ch] += db[b][j];
-                ub += (long long)P.ay[b] * S[b][ch];
-              }
-            }
-            Ubuf[ch * UPITCH + tid] = (int)(ua >> P.ushift);
-            Ubuf[(nch + ch) * UPITCH + tid] = (int)(ub >> P.ushift);
-          }
+          for (int t = 0; t < 4; ++t) Ubuf[(4 * i + t) * UP + tid] = U[4 * i + t] >> P.ush;
         }
       }
     }
-    __syncthreads();
-
-    // ---------------------------------------------------------------- H: horizontal slide
-    // Each walker (row, channel, segment) slides the exact int32 box sums H_b of U' along the
-    // row and writes F = (sum_b ax_b H_b) >> fshift (exact int64 product sum, narrowed).
-    if (wr < R && wch < nch && ya + wr < yend) {
-      const int xs = wseg * seglen;
-      const int xe = min(xs + seglen, TWv);
-      if (xs < xe) {
-        const int* Ur = Ubuf + (wr * nch + wch) * UPITCH + P.rlo_x;
-        int* Fr = Fbuf + (wr * nch + wch) * FPITCH;
-        int Hs[NB];
-#pragma unroll
-        for (int b = 0; b < NB; ++b) Hs[b] = (b < P.nbx) ? range_sum(Ur, xs + P.lox[b], xs + P.hix[b]) : 0;
-        Fr[xs] = combine_boxes<NB>(Hs, P);
-        const int* pe[NB];
-        const int* pl[NB];
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          pe[b] = Ur + xs + 1 + P.hix[b];
-          pl[b] = Ur + xs + P.lox[b];
-        }
-        int x = xs + 1;
-        for (; x + 7 < xe; x += 8) {
-          int e[NB][8], l[NB][8];
-#pragma unroll
-          for (int b = 0; b < NB; ++b)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              e[b][j] = pe[b][j];
-              l[b][j] = pl[b][j];
-            }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-#pragma unroll
-            for (int b = 0; b < NB; ++b) Hs[b] += e[b][j] - l[b][j];
-            Fr[x + j] = combine_boxes<NB>(Hs, P);
-          }
-#pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            pe[b] += 8;
-            pl[b] += 8;
-          }
-        }
-        for (; x < xe; ++x) {
-#pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            Hs[b] += pe[b][0] - pl[b][0];
-            pe[b] += 1;
-            pl[b] += 1;
-          }
-          Fr[x] = combine_boxes<NB>(Hs, P);
-        }
+    // ------------------------------------------------------------ C(y-1): combine, normalise
+    // num = sum_k W_c F_Ic + W_s F_Is, den = sum_k W_c F_c + W_s F_s with the weights
+    // a_k cos / sin(k pi I(x) / D) computed in fp64 and rounded to integers (exact int64 sums).
+    if (y > y0 && tid < TWv) {
+      double c1, s1;
+      if (U8) {
+        const double2 t = lut64[(int)Ic];
+        c1 = t.x;
+        s1 = t.y;
+      } else {
+        base_angle_f64(Ic, P.invD, c1, s1);
       }
-    }
-    __syncthreads();
-
-    // ---------------------------------------------------------------- C: combine, divide
-    // num = sum_k a_k (cos F_Ic + sin F_Is), den = sum_k a_k (cos F_c + sin F_s) with the weights
-    // quantised to WBITS and the products accumulated exactly in int64 (an fp32 combine of the
-    // box sums loses the tolerance at ill-conditioned pixels).
-    for (int o = tid; o < R * TWv; o += NT) {
-      const int r = o / TWv, xo = o - r * TWv;
-      const int y = ya + r;
-      if (y >= yend) continue;
-      const long long pix = fbase + (long long)y * P.W + (x0 + xo);
-      const int* Fr = Fbuf + r * nch * FPITCH + xo;
-      float c1, s1, I;
-      bool valid;
-      tap_base<U8>(in, P, lut, y, x0 + xo, fbase, c1, s1, I, valid);
-      float c = 1.f, s = 0.f;
-      for (int j = 0; j < P.k0; ++j) rotate(c, s, c1, s1);
+      Cheb64 g;
+      g.init(c1, s1);
+      for (int j = 0; j < P.kstep[0]; ++j) g.step();
       long long num = 0, den = 0;
+      const int4* Fr = reinterpret_cast<const int4*>(Fbuf + tid * FPX);
 #pragma unroll
       for (int i = 0; i < MAXK; ++i) {
-        if (i < P.nk) {
-          if (CONSEC) {
-            if (i > 0) rotate(c, s, c1, s1);
-          } else {
-            for (int j = 0; j < P.kstep[i]; ++j) rotate(c, s, c1, s1);
+        if (FULL || i < nk) {
+          if (i > 0) {
+            if (CONSEC) g.step();
+            else
+              for (int j = 0; j < P.kstep[i]; ++j) g.step();
           }
-          const long long wc = __float2int_rn(P.aw[i] * c), wsn = __float2int_rn(P.aw[i] * s);
-          den += wc * Fr[(4 * i) * FPITCH] + wsn * Fr[(4 * i + 1) * FPITCH];
-          num += wc * Fr[(4 * i + 2) * FPITCH] + wsn * Fr[(4 * i + 3) * FPITCH];
+          const int wc = __double2loint(fma(g.c, P.aw[i], MAGIC64));
+          const int wsn = __double2loint(fma(g.s, P.aw[i], MAGIC64));
+          const int4 f = Fr[i];   // (F_c, F_s, F_Ic, F_Is) of term i
+          den += (long long)wc * f.x;
+          den += (long long)wsn * f.y;
+          num += (long long)wc * f.z;
+          num += (long long)wsn * f.w;
         }
       }
+      const long long pix = fbase + (long long)(y - 1) * P.W + x0 + tid;
       if (P.pass == 1) {
         ws[pix] = make_longlong2(num, den);
       } else {
@@ -456,57 +399,97 @@ __global__ void __launch_bounds__(NT, 1) bf_strip_kernel(const KParams P, const 
           num += acc.x;
           den += acc.y;
         }
-        if (P.pass == 2) {
-          ws[pix] = make_longlong2(num, den);
-        } else {
-          out[pix] = (den > 0) ? (float)((double)P.D * (double)num / (double)den) : I;
+        if (P.pass == 2) ws[pix] = make_longlong2(num, den);
+        else out[pix] = (den > 0) ? (float)(P.D * (double)num / (double)den) : Ic;
+      }
+    }
+    if (y >= yend) break;
+    if (tid < TWv) Ic = load_pixel(in, U8, fbase + (long long)y * P.W + x0 + tid);
+    __syncthreads();
+
+    // ============================================================ interval B: H(y)
+    // Walkers slide the exact int32 horizontal box sums H_b of U' along the row and write
+    // F = (sum_b ax_b H_b + frnd) >> fsh (exact int64 product sum, narrowed). Lanes of a warp
+    // are 32 channels at the same x: conflict-free reads (pitch == 1 mod 32) and writes.
+    if (wact) {
+      const int xs = wseg * P.seglen;
+      const int xe = min(xs + P.seglen, TWv);
+      if (xs < xe) {
+        const int* Ur = Ubuf + wslot * UP + P.rlo_x;   // Ur[o + u]: U' at output column o, offset u
+        int* Fr = Fbuf + wslot;   // Fr[x * FPX]
+        int hlo[NB], hhi[NB], ax[NB];
+        int Hs[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          hlo[b] = P.hlo[b];
+          hhi[b] = P.hhi[b];
+          ax[b] = (b < P.nbx) ? P.ax[b] : 0;
+        }
+        // initial window sums at xs; a box nested in its predecessor reuses the inner sum
+#pragma unroll
+        for (int b = NB - 1; b >= 0; --b) {
+          Hs[b] = 0;
+          if (b < P.nbx) {
+            int lo = xs + hlo[b], hi = xs + hhi[b];
+            int acc = 0, lo2 = hi + 1, hi2 = hi;
+            if (b + 1 < NB && b + 1 < P.nbx && hlo[b] <= hlo[b + 1] && hhi[b + 1] <= hhi[b]) {
+              acc = Hs[b + 1];
+              lo2 = xs + hhi[b + 1] + 1;
+              hi = xs + hlo[b + 1] - 1;
+            }
+            int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll 1
+            for (int pass = 0; pass < 2; ++pass) {
+              int j = pass ? lo2 : lo;
+              const int je = pass ? hi2 : hi;
+              for (; j + 3 <= je; j += 4) {
+                a0 += Ur[j];
+                a1 += Ur[j + 1];
+                a2 += Ur[j + 2];
+                a3 += Ur[j + 3];
+              }
+              for (; j <= je; ++j) a0 += Ur[j];
+            }
+            Hs[b] = acc + (a0 + a1) + (a2 + a3);
+          }
+        }
+        const long long frnd = P.frnd;
+        const int fsh = P.fsh;
+        int x = xs;
+        for (; x + 4 <= xe; x += 4) {
+          int e[NB][4], l[NB][4];
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              e[b][j] = Ur[x + j + 1 + hhi[b]];
+              l[b][j] = Ur[x + j + hlo[b]];
+            }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            long long f = frnd;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) f += (long long)ax[b] * Hs[b];
+            Fr[(x + j) * FPX] = (int)(f >> fsh);
+#pragma unroll
+            for (int b = 0; b < NB; ++b) Hs[b] += e[b][j] - l[b][j];
+          }
+        }
+        for (; x < xe; ++x) {
+          long long f = frnd;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) f += (long long)ax[b] * Hs[b];
+          Fr[x * FPX] = (int)(f >> fsh);
+#pragma unroll
+          for (int b = 0; b < NB; ++b) Hs[b] += Ur[x + 1 + hhi[b]] - Ur[x + hlo[b]];
         }
       }
     }
-    // the next iteration's V phase only writes Ubuf, which no thread reads after the H phase
+    __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------ host side
-
-struct LaunchShape {
-  int NT, MAXK, TW, TH, passes;
-};
-
-template <int MAXK, bool U8, int NT, bool CONSEC, int NB>
-cudaError_t launch_one(const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid, cudaStream_t st) {
-  constexpr int C = 4 * MAXK;
-  const size_t nch = 4 * (size_t)P.nk;
-  size_t smem = 2 * (nch * (NT + 1) * 4 + nch * (P.TW + 1) * 4) + 256 * sizeof(float2);
-  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  auto kfn = bf_strip_kernel<MAXK, U8, NT, CONSEC, NB>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kfn<<<grid, NT, smem, st>>>(P, in, out, ws);
-  return cudaGetLastError();
-}
-
-template <int MAXK, bool U8, int NT>
-cudaError_t dispatch_shape(bool consec, int nb, const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid,
-                           cudaStream_t st) {
-  if (consec) {
-    if (nb == 1) return launch_one<MAXK, U8, NT, true, 1>(P, in, out, ws, grid, st);
-    if (nb == 2) return launch_one<MAXK, U8, NT, true, 2>(P, in, out, ws, grid, st);
-  } else {
-    if (nb == 1) return launch_one<MAXK, U8, NT, false, 1>(P, in, out, ws, grid, st);
-    if (nb == 2) return launch_one<MAXK, U8, NT, false, 2>(P, in, out, ws, grid, st);
-  }
-  return launch_one<MAXK, U8, NT, false, 4>(P, in, out, ws, grid, st);
-}
-
-template <bool U8>
-cudaError_t dispatch(int NT, int MAXK, bool consec, int nb, const KParams& P, const void* in, float* out, longlong2* ws,
-                     dim3 grid, cudaStream_t st) {
-  if (NT == 256 && MAXK == 8) return dispatch_shape<8, U8, 256>(consec, nb, P, in, out, ws, grid, st);
-  if (NT == 256 && MAXK == 16) return dispatch_shape<16, U8, 256>(consec, nb, P, in, out, ws, grid, st);
-  if (NT == 512 && MAXK == 8) return dispatch_shape<8, U8, 512>(consec, nb, P, in, out, ws, grid, st);
-  return cudaErrorInvalidConfiguration;
-}
 
 int sm_count() {
   static int n = 0;
@@ -518,102 +501,162 @@ int sm_count() {
   return n;
 }
 
+size_t smem_layout(KParams& P, int NT, int MAXK, bool u8) {
+  auto up16 = [](size_t v) { return (v + 15) / 16 * 16; };
+  size_t off = up16(sizeof(int) * 4 * (size_t)P.nk * (NT + 1));
+  P.f_off = (int)off;
+  off = up16(off + sizeof(int) * (size_t)P.TW * (4 * MAXK + 4));
+  P.l_off = (int)off;
+  if (u8) off += 256 * (sizeof(float2) + sizeof(double2));
+  return off;
+}
+
+template <int MAXK, int NB, bool U8, int NT, bool CONSEC, bool FULL = false>
+cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim3 grid, cudaStream_t st) {
+  auto kfn = bf_band_kernel<MAXK, NB, U8, NT, CONSEC, FULL>;
+  const size_t smem = smem_layout(P, NT, MAXK, U8);
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kfn<<<grid, NT, smem, st>>>(P, in, out, ws);
+  return cudaGetLastError();
+}
+
+template <int MAXK, bool U8, int NT>
+cudaError_t dispatch_nb(int nb, bool consec, const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid,
+                        cudaStream_t st) {
+  const bool full = consec && P.nk == MAXK;
+  if (nb <= 1) return full ? launch_one<MAXK, 1, U8, NT, true, true>(P, in, out, ws, grid, st)
+                    : consec ? launch_one<MAXK, 1, U8, NT, true>(P, in, out, ws, grid, st)
+                             : launch_one<MAXK, 1, U8, NT, false>(P, in, out, ws, grid, st);
+  if (nb == 2) return full ? launch_one<MAXK, 2, U8, NT, true, true>(P, in, out, ws, grid, st)
+                    : consec ? launch_one<MAXK, 2, U8, NT, true>(P, in, out, ws, grid, st)
+                             : launch_one<MAXK, 2, U8, NT, false>(P, in, out, ws, grid, st);
+  return launch_one<MAXK, 4, U8, NT, false>(P, in, out, ws, grid, st);
+}
+
+struct Shape {
+  int NT, MAXK;
+};
+
+// Thread-block shape per plan: NT extended columns (TW = NT - halo outputs, TW >= NT/2 where
+// possible) and MAXK terms per pass (the vertical state is 4*MAXK registers per thread).
+Shape choose_shape(int halo, int nk) {
+  Shape sh = halo <= 128 ? Shape{256, nk <= 8 ? 8 : 16} : Shape{512, 8};
+  if (const char* e = std::getenv("BF_MAXK")) sh.MAXK = std::atoi(e) <= 8 ? 8 : 16;   // tuning hook
+  if (sh.NT == 512) sh.MAXK = 8;
+  return sh;
+}
+
+template <bool U8>
+cudaError_t dispatch(const Shape& sh, int nb, bool consec, const KParams& P, const void* in, float* out,
+                     longlong2* ws, dim3 grid, cudaStream_t st) {
+  if (sh.NT == 256 && sh.MAXK == 8) return dispatch_nb<8, U8, 256>(nb, consec, P, in, out, ws, grid, st);
+  if (sh.NT == 256 && sh.MAXK == 16) return dispatch_nb<16, U8, 256>(nb, consec, P, in, out, ws, grid, st);
+  if (sh.NT == 512 && sh.MAXK == 8) return dispatch_nb<8, U8, 512>(nb, consec, P, in, out, ws, grid, st);
+  return cudaErrorInvalidConfiguration;
+}
+
 bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_frames, int H, int W,
                      cudaStream_t st) {
   if (!p || !d_in || !d_out || H <= 0 || W <= 0 || n_frames <= 0) return BF_ERR_INVALID_ARG;
   if ((long long)H * W > (1LL << 40) / n_frames) return BF_ERR_INVALID_ARG;
   if ((const void*)d_out == d_in) return BF_ERR_INVALID_ARG;
-  if (!p->separable || p->nbx > MAXB || p->nby > MAXB) return BF_ERR_UNSUPPORTED;
+  if (!p->separable || p->nbx > MAXB || p->nby > MAXB || p->nbx < 1 || p->nby < 1) return BF_ERR_UNSUPPORTED;
   int rlo = 0, rhi = 0;
   for (int b = 0; b < p->nbx; ++b) {
     rlo = std::max(rlo, -p->lox[b]);
     rhi = std::max(rhi, p->hix[b]);
   }
   const int halo = rlo + rhi;
-  int NT;
-  if (halo + 32 <= 256) NT = 256;
-  else if (halo + 64 <= 512) NT = 512;
-  else return BF_ERR_UNSUPPORTED;
-  const int TW = NT - halo;
-  // channels per launch: as many as fit the registers (MAXK) and the two-row shared-memory
-  // buffers (2 rows x nch x (NT + 1 + TW + 1) ints); otherwise several accumulating launches
-  auto smem_for = [&](int nk) { return 2 * (4.0 * nk * (NT + 1) * 4 + 4.0 * nk * (TW + 1) * 4) + 2048; };
-  int MAXK = (NT == 512) ? 8 : (p->n_k <= 8 ? 8 : 16);
-  while (MAXK > 8 && smem_for(std::min(MAXK, p->n_k)) > 227.0 * 1024) MAXK = 8;
-  if (smem_for(std::min(MAXK, p->n_k)) > 227.0 * 1024) return BF_ERR_UNSUPPORTED;
-  const int passes = (p->n_k + MAXK - 1) / MAXK;
+  const Shape sh = choose_shape(halo, p->n_k);
+  if (halo + 32 > sh.NT) return BF_ERR_UNSUPPORTED;
+  const int TW = sh.NT - halo;
+  const int passes = (p->n_k + sh.MAXK - 1) / sh.MAXK;
   const int nstrips = (W + TW - 1) / TW;
-  // band height: whole waves of 1-CTA-per-SM work, init (2r+1 rows) amortised over >= 4r rows
-  const int nsm = sm_count();
-  int ry = 0;
-  for (int b = 0; b < p->nby; ++b) ry = std::max(ry, p->hiy[b] - p->loy[b] + 1);
-  long long best_cost = -1;
-  int best_nb = 1;
-  for (int nb = 1; nb <= H; ++nb) {
-    int TH = (H + nb - 1) / nb;
-    if (nb > 1 && TH < 32) break;
-    long long ctas = (long long)nstrips * nb * n_frames;
-    long long waves = (ctas + nsm - 1) / nsm;
-    long long cost = waves * (4LL * TH + ry);
-    if (best_cost < 0 || cost < best_cost) {
-      best_cost = cost;
-      best_nb = nb;
-    }
-  }
-  const int TH = (H + best_nb - 1) / best_nb;
-  best_nb = (H + TH - 1) / TH;
 
   KParams P;
   std::memset(&P, 0, sizeof(P));
   P.H = H;
   P.W = W;
+  P.frame_elems = (long long)H * W;
+  P.TW = TW;
+  P.rlo_x = rlo;
   P.nbx = p->nbx;
   P.nby = p->nby;
-  double wxmax = 0.0;
-  for (int b = 0; b < p->nbx; ++b) wxmax = std::max(wxmax, std::fabs(p->wx[b]));
-  for (int b = 0; b < p->nbx; ++b) {
-    P.lox[b] = p->lox[b];
-    P.hix[b] = p->hix[b];
-    P.ax[b] = (int)std::lround(std::ldexp(p->wx[b] / wxmax, ABITS));
-  }
-  // vertical box weights as integers; S_b bounded by n_b * (QMAX + 1/2)
-  double wymax = 0.0;
+  // ---- vertical: scales wy_b / max|wy| * 2^q, q as large as the int32 state allows
+  double wymax = 0.0, wsum = 0.0;
   for (int b = 0; b < p->nby; ++b) wymax = std::max(wymax, std::fabs(p->wy[b]));
-  double sbound = 0.0;  // bound of |sum_b ay_b S_b|
-  P.vlo = p->loy[0];
-  P.vhi = p->hiy[0];
+  for (int b = 0; b < p->nby; ++b) wsum += std::fabs(p->wy[b]) / wymax * (p->hiy[b] - p->loy[b] + 1);
+  int qb = QBITS_MAX;
+  while (qb > 8 && std::ldexp(wsum, qb) + 4.0 * (p->hiy[0] - p->loy[0] + 8) >= 2147483647.0 - 65536.0) --qb;
+  double ubound = 0.0;   // bound of |U| before the shift
+  P.vmin = p->loy[0];
+  P.vmax = p->hiy[0];
   for (int b = 0; b < p->nby; ++b) {
-    P.loy[b] = p->loy[b];
-    P.hiy[b] = p->hiy[b];
-    P.ay[b] = (int)std::lround(std::ldexp(p->wy[b] / wymax, ABITS));
-    sbound += std::fabs((double)P.ay[b]) * ((double)QMAX + 0.5) * (p->hiy[b] - p->loy[b] + 1);
-    P.vlo = std::min(P.vlo, p->loy[b]);
-    P.vhi = std::max(P.vhi, p->hiy[b]);
-    if ((p->hiy[b] - p->loy[b] + 1) * ((double)QMAX + 0.5) >= 2147483647.0) return BF_ERR_UNSUPPORTED;
+    P.vlo[b] = p->loy[b];
+    P.vhi[b] = p->hiy[b];
+    P.qs[b] = (float)std::ldexp(p->wy[b] / wymax, qb);
+    P.qsD[b] = (float)((double)P.qs[b] / p->D);
+    ubound += (std::fabs((double)P.qs[b]) + 0.5) * (p->hiy[b] - p->loy[b] + 1);
+    P.vmin = std::min(P.vmin, p->loy[b]);
+    P.vmax = std::max(P.vmax, p->hiy[b]);
   }
-  P.qD = (float)((double)QMAX / p->D);
-  // U' = S >> ushift so that every horizontal box sum of U' stays inside int32
   int nxmax = 1;
   for (int b = 0; b < p->nbx; ++b) nxmax = std::max(nxmax, p->hix[b] - p->lox[b] + 1);
-  P.ushift = 0;
-  while ((sbound / std::ldexp(1.0, P.ushift) + 1.0) * nxmax >= 2147483647.0) ++P.ushift;
-  {
-    // bound of |sum_b ax_b H_b| -> shift that narrows F to int32
-    const double ub = sbound / std::ldexp(1.0, P.ushift) + 1.0;
-    double fb = 0.0;
-    for (int b = 0; b < p->nbx; ++b) fb += std::fabs((double)P.ax[b]) * ub * (p->hix[b] - p->lox[b] + 1);
-    P.fshift = 0;
-    while (fb / std::ldexp(1.0, P.fshift) >= 2147483000.0) ++P.fshift;
+  P.ush = 0;
+  while ((ubound / std::ldexp(1.0, P.ush) + 1.0) * nxmax >= 2147483000.0) ++P.ush;
+  P.urnd = P.ush > 0 ? (1 << (P.ush - 1)) : 0;
+  // ---- horizontal: integer weights, F narrowed to int32
+  double wxmax = 0.0;
+  for (int b = 0; b < p->nbx; ++b) wxmax = std::max(wxmax, std::fabs(p->wx[b]));
+  const double uprime = ubound / std::ldexp(1.0, P.ush) + 1.0;
+  double fb = 0.0;
+  for (int b = 0; b < p->nbx; ++b) {
+    P.hlo[b] = p->lox[b];
+    P.hhi[b] = p->hix[b];
+    P.ax[b] = (int)std::lround(std::ldexp(p->wx[b] / wxmax, ABITS));
+    fb += std::fabs((double)P.ax[b]) * uprime * (p->hix[b] - p->lox[b] + 1);
   }
-  P.rlo_x = rlo;
-  P.TW = TW;
-  P.TH = TH;
+  P.fsh = 0;
+  while (fb / std::ldexp(1.0, P.fsh) >= 2147483000.0) ++P.fsh;
+  P.frnd = P.fsh > 0 ? (1LL << (P.fsh - 1)) : 0;
+  // ---- combine weights a_k * 2^wbits: |W| < 2^31 and |num|, |den| < 2^62
+  double asum = 0.0, amax = 0.0;
+  for (int i = 0; i < p->n_k; ++i) {
+    asum += std::fabs(p->a[i]);
+    amax = std::max(amax, std::fabs(p->a[i]));
+  }
+  int wbits = 29;
+  while (wbits > 8 && (std::ldexp(asum, wbits) * 2.0 * 2147483648.0 >= 4.0e18 || std::ldexp(amax, wbits) >= 2.0e9))
+    --wbits;
   const double invD = 1.0 / p->D;
+  P.invD = invD;
   P.invD_hi = (float)invD;
   P.invD_lo = (float)(invD - (double)P.invD_hi);
-  P.D = (float)p->D;
-  P.frame_elems = (long long)H * W;
-  const int nbmax = std::max(p->nbx, p->nby);
+  P.D = p->D;
+
+  // ---- band height: CTAs in whole waves of the resident slots, init (vmax - vmin + 1 rows)
+  //      amortised over the band
+  const int nsm = sm_count();
+  const int slots = nsm * (sh.NT > 256 ? 1 : 2);
+  const int ry = P.vmax - P.vmin + 1;
+  long long best_cost = -1;
+  int best_nb = 1;
+  for (int nb = 1; nb <= H; ++nb) {
+    const int TH = (H + nb - 1) / nb;
+    if (nb > 1 && TH < 16) break;
+    const long long ctas = (long long)nstrips * nb * n_frames;
+    const long long waves = (ctas + slots - 1) / slots;
+    const long long cost = waves * (4LL * TH + ry);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best_nb = nb;
+    }
+  }
+  P.TH = (H + best_nb - 1) / best_nb;
+  best_nb = (H + P.TH - 1) / P.TH;
+
   longlong2* ws = nullptr;
   if (passes > 1) {
     if (cudaMallocAsync(&ws, sizeof(longlong2) * (size_t)H * W * n_frames, st) != cudaSuccess) return BF_ERR_CUDA;
@@ -623,22 +666,31 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
   cudaError_t err = cudaSuccess;
   int prevk = 0;
   for (int pass = 0; pass < passes && err == cudaSuccess; ++pass) {
-    const int first = pass * MAXK;
-    const int nk = std::min(MAXK, p->n_k - first);
+    const int first = pass * sh.MAXK;
+    const int nk = std::min(sh.MAXK, p->n_k - first);
     P.nk = nk;
-    P.k0 = prevk;
+    P.ngrp = (4 * nk + 31) / 32;
+    bool consec = true;
     for (int i = 0; i < nk; ++i) {
-      int kk = p->k[first + i];
-      P.kstep[i] = kk - (i == 0 ? prevk : p->k[first + i - 1]);
-      P.a[i] = (float)p->a[first + i];
-      P.aw[i] = (float)std::ldexp(p->a[first + i], WBITS);
+      const int kk = p->k[first + i];
+      P.kstep[i] = (i == 0) ? kk : kk - p->k[first + i - 1];
+      if (i > 0 && P.kstep[i] != 1) consec = false;
+      P.aw[i] = std::ldexp(p->a[first + i], wbits);
     }
-    prevk = p->k[first + nk - 1];
+    (void)prevk;
+    // walker segments: ngrp * nseg warps <= NT / 32; long segments amortise the initial window
+    // sums (2r+1 reads per box)
+    const int max_tasks = sh.NT / 32;
+    int nseg = std::max(1, max_tasks / P.ngrp);
+    const int min_len = std::max(32, 2 * (rlo + rhi + 1) / 3);
+    while (nseg > 1 && (TW + nseg - 1) / nseg < min_len) --nseg;
+    if (const char* e = std::getenv("BF_NSEG")) nseg = std::max(1, std::min(max_tasks / P.ngrp, std::atoi(e)));  // tuning hook
+    P.nseg = nseg;
+    P.seglen = (TW + nseg - 1) / nseg;
     P.pass = (passes == 1) ? 0 : (pass == 0 ? 1 : (pass == passes - 1 ? 3 : 2));
-    bool consec = (P.k0 == 0);
-    for (int i = 0; i < nk; ++i) consec = consec && (p->k[first + i] == i);
-    err = u8 ? dispatch<true>(NT, MAXK, consec, nbmax, P, d_in, d_out, ws, grid, st)
-             : dispatch<false>(NT, MAXK, consec, nbmax, P, d_in, d_out, ws, grid, st);
+    const int nb = std::max(p->nbx, p->nby);
+    err = u8 ? dispatch<true>(sh, nb, consec, P, d_in, d_out, ws, grid, st)
+             : dispatch<false>(sh, nb, consec, P, d_in, d_out, ws, grid, st);
   }
   if (ws) cudaFreeAsync(ws, st);
   return err == cudaSuccess ? BF_OK : BF_ERR_CUDA;

@@ -1,0 +1,4 @@
+set -x
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | cut -c1-400
+for c in cfg0 cfg1 cfg3 cfg4; do timeout 300 python bench.py --steps 5 --warmup 3 --config $c --no-cpu-baseline 2>&1 | tail -1 | cut -c1-250; done
