@@ -40,28 +40,48 @@ def measured_peaks() -> dict:
 
 
 class ClockSampler:
-    """Samples nvidia-smi clocks / throttle reasons every 200 ms while the timed region runs."""
+    """Samples SM clocks and clock-event (throttle) reasons while the timed region runs: NVML every
+    20 ms (nvidia_ml_py), else nvidia-smi every 200 ms."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []      # (sm_mhz, max_mhz, power_w, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml:
+            nv, h = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            return (float(sm), float(mx), pw, int(rs))
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        c = [x.strip() for x in out.stdout.strip().split(",")]
+        mask = sum(bit for bit, v in zip((0x8, 0x40, 0x20, 0x4), c[3:7]) if v.lower() == "active")
+        return (float(c[0]), float(c[1]), float(c[2]) if c[2].replace(".", "").isdigit() else 0.0, mask)
 
     def _loop(self):
+        period = 0.02 if self._nvml else 0.2
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+                self.rows.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(period)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._loop, daemon=True)
@@ -75,14 +95,11 @@ class ClockSampler:
 
     def summary(self) -> dict:
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.strip().lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": reasons, "samples": len(self.rows),
-                "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
+        reasons = sorted({n for r in self.rows for n, bit in self.NAMES.items() if r[3] & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(r[2] for r in self.rows),
+                "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def dist_setup(n_gpus: int):
@@ -168,6 +185,15 @@ def run_reference(args, spec):
 # our arm
 # --------------------------------------------------------------------------------------------
 
+def traffic_per_launch(cfg: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p)).get(cfg, {}).get("dram_bytes_per_launch")
+
+
 def run_ours(args, spec):
     import torch
     from paper_1803_00004_b200 import build
@@ -189,7 +215,7 @@ def run_ours(args, spec):
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
     H, W = img.shape
-    passes = (len(plan.info()["k"]) + 7) // 8 if spec.radius > 100 else (1 if len(plan.info()["k"]) <= 16 else 2)
+    launches = bfp.launches(plan, H, W)     # kernel launches per bf_apply (bf_apply_launches)
 
     def step():
         bfp.apply(plan, img.data_ptr(), out.data_ptr(), H, W, sptr)
@@ -238,26 +264,36 @@ def run_ours(args, spec):
     peaks = measured_peaks()
     bytes_per_px = (1 if u8 else 4) + 4
     alg_bytes = H * W * bytes_per_px
-    achieved_gbs = alg_bytes / (ms / 1e3) / 1e9
+    hbm_gbs = alg_bytes / (ms / 1e3) / 1e9
     hbm_peak = float(peaks["hbm_gbs"])
     clocks = sampler.summary()
     nk = len(plan.info()["k"])
     C = 4 * nk
+    # ALU roofline (the bound of this path): SURVEY 8(d)'s algorithmic work of
+    # >= 8 FP32-lane ops per box-filtered channel per pixel, against 148 SMs x 128 FP32 lanes x the
+    # SM clock measured under load (max clock if nvidia-smi gave none)
+    sm_mhz = clocks.get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
+    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12                  # T lane-op/s
+    alu_ops = 8.0 * C * H * W                                    # per step
+    alu_achieved = alu_ops / (ms / 1e3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 channels / exact i32 box sums / f64 combine", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32 channels, i32 box sums, i64 combine", "data": "synthetic",
         "config": config_dict(spec, True, world),
-        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved_gbs / hbm_peak, "traffic": args.traffic,
-                     "kernel": "bf_strip_kernel", "algorithmic_bytes_per_launch": alg_bytes,
-                     "peak_source": peaks["_source"] + " hbm_gbs",
-                     "note": "the kernel is ALU/issue bound, not HBM bound (DESIGN.md roofline)"},
-        "alu_roofline": {"channel_pixels_per_s": C * H * W / (ms / 1e3), "channels": C,
-                         "note": "see DESIGN.md for the per channel-pixel instruction floor"},
+        "roofline": {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "T lane-op/s",
+                     "frac": alu_achieved / alu_peak, "traffic": traffic_per_launch(spec.name),
+                     "kernel": "bf_band_kernel", "launches_per_step": launches,
+                     "algorithmic_ops_per_step": alu_ops,
+                     "peak_source": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (B200_PROFILING.md unit counts)",
+                     "note": "SURVEY 8(d): >= 8 FP32-lane ops per channel-pixel, C = 4 N_eff channels"},
+        "hbm_roofline": {"achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_gbs / hbm_peak,
+                         "algorithmic_bytes_per_step": alg_bytes,
+                         "peak_source": peaks["_source"] + " hbm_gbs",
+                         "note": "BASELINE metric: image bytes in + out at the measured HBM bandwidth"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(img_np.nbytes),
                 "d2h_bytes_per_step": int(H * W * 4)},
-        "gpu_launches": args.steps * passes,
+        "gpu_launches": args.steps * launches,
         "clocks": clocks,
     }
     if not args.no_cpu_baseline:
@@ -276,8 +312,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-side", type=int, default=512, help="side of the oracle's timed crop")
-    ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch, if measured")
+    ap.add_argument("--ref-side", type=int, default=768, help="side of the oracle's timed crop")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     from synth import CONFIGS

@@ -150,6 +150,14 @@ BF_API bf_status bf_apply_batched(const bf_plan* plan, const void* d_in, float* 
  * from a library-owned cache keyed by size (grown on demand, freed at exit). */
 BF_API bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float* h_out, int H, int W, bf_stream stream);
 
+/*
+ * Number of kernel launches one bf_apply / bf_apply_batched of an H x W image enqueues with this
+ * plan (the range terms run in ceil(N_eff / terms-per-pass) passes; several passes accumulate
+ * num / den in an int64 workspace). Pure host computation, no device work. Returns
+ * BF_ERR_INVALID_ARG for a NULL plan / pointer or H, W <= 0, BF_ERR_UNSUPPORTED as bf_apply would.
+ */
+BF_API bf_status bf_apply_launches(const bf_plan* plan, int H, int W, int* n_launches);
+
 /* Static string for a status code. */
 BF_API const char* bf_status_string(bf_status s);
 

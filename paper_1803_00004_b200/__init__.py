@@ -10,9 +10,10 @@ streams; every step of the filter runs in the library's host fitter and sm_100a 
 """
 from __future__ import annotations
 
-from ._bf import (BFError, Plan, apply, apply_batched, apply_host, lib, version)
+from ._bf import (BFError, Plan, apply, apply_batched, apply_host, launches, lib, version)
 
-__all__ = ["BFError", "Plan", "apply", "apply_batched", "apply_host", "bilateral_filter", "lib", "version"]
+__all__ = ["BFError", "Plan", "apply", "apply_batched", "apply_host", "bilateral_filter", "launches", "lib",
+           "version"]
 
 
 def _check_tensor(t, plan):

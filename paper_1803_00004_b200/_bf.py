@@ -23,7 +23,7 @@ RANGE = {"gaussian": BF_RANGE_GAUSSIAN, "tukey": BF_RANGE_TUKEY}
 
 #: every symbol include/bf.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bf_plan_options_default", "bf_plan_create", "bf_plan_destroy", "bf_plan_get_info", "bf_apply",
-           "bf_apply_batched", "bf_apply_host", "bf_status_string", "bf_version")
+           "bf_apply_batched", "bf_apply_host", "bf_apply_launches", "bf_status_string", "bf_version")
 
 
 class PlanOptions(C.Structure):
@@ -80,6 +80,8 @@ def lib() -> C.CDLL:
         L.bf_apply_batched.restype = C.c_int
         L.bf_apply_host.argtypes = [P, P, P, C.c_int, C.c_int, P]
         L.bf_apply_host.restype = C.c_int
+        L.bf_apply_launches.argtypes = [P, C.c_int, C.c_int, C.POINTER(C.c_int)]
+        L.bf_apply_launches.restype = C.c_int
         L.bf_status_string.argtypes = [C.c_int]
         L.bf_status_string.restype = C.c_char_p
         L.bf_version.argtypes = []
@@ -159,6 +161,13 @@ def apply_host(plan: Plan, h_in: int, h_out: int, H: int, W: int, stream: int = 
     """bf_apply_host on raw host pointers (copies in, filters, copies out, synchronises)."""
     _check(lib().bf_apply_host(plan.handle, C.c_void_p(h_in), C.c_void_p(h_out), int(H), int(W), C.c_void_p(stream)),
            "bf_apply_host")
+
+
+def launches(plan: Plan, H: int, W: int) -> int:
+    """Kernel launches one bf_apply of an H x W image enqueues (bf_apply_launches)."""
+    n = C.c_int(0)
+    _check(lib().bf_apply_launches(plan.handle, int(H), int(W), C.byref(n)), "bf_apply_launches")
+    return n.value
 
 
 def version() -> str:

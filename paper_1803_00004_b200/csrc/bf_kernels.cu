@@ -712,6 +712,21 @@ HostCache g_cache;
 
 }  // namespace
 
+extern "C" bf_status bf_apply_launches(const bf_plan* p, int H, int W, int* n) {
+  if (!p || !n || H <= 0 || W <= 0) return BF_ERR_INVALID_ARG;
+  *n = 0;
+  if (!p->separable || p->nbx > MAXB || p->nby > MAXB || p->nbx < 1 || p->nby < 1) return BF_ERR_UNSUPPORTED;
+  int rlo = 0, rhi = 0;
+  for (int b = 0; b < p->nbx; ++b) {
+    rlo = std::max(rlo, -p->lox[b]);
+    rhi = std::max(rhi, p->hix[b]);
+  }
+  const Shape sh = choose_shape(rlo + rhi, p->n_k);
+  if (rlo + rhi + 32 > sh.NT) return BF_ERR_UNSUPPORTED;
+  *n = (p->n_k + sh.MAXK - 1) / sh.MAXK;
+  return BF_OK;
+}
+
 extern "C" bf_status bf_apply(const bf_plan* plan, const void* d_in, float* d_out, int H, int W, bf_stream stream) {
   return run_filter(plan, d_in, d_out, 1, H, W, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -30,7 +30,7 @@ def header_functions():
 def test_header_declares_expected_api():
     assert header_functions() == sorted(["bf_plan_options_default", "bf_plan_create", "bf_plan_destroy",
                                          "bf_plan_get_info", "bf_apply", "bf_apply_batched", "bf_apply_host",
-                                         "bf_status_string", "bf_version"])
+                                         "bf_apply_launches", "bf_status_string", "bf_version"])
 
 
 def test_library_exports_every_declared_symbol(bfmod):
@@ -118,3 +118,19 @@ def test_plan_edge_parameters(bfmod):
     assert r0["boxes_x"] == [(0, 0, r0["boxes_x"][0][2])] and r0["separable"]
     box = bfmod.Plan(spatial="box", radius=10).info()
     assert len(box["spatial_terms"]) == 1 and box["boxes_x"][0][:2] == (-10, 10)
+
+
+def test_launch_count_query(bfmod):
+    """bf_apply_launches: one launch when the terms fit one pass, ceil(N / 8) at r = 192 (cfg4),
+    argument validation; host-only (no device work)."""
+    import ctypes as C
+    L = bfmod.lib()
+    for cfg, want in (("cfg0", 1), ("cfg2", 1), ("cfg3", 1), ("cfg4", 3)):
+        p = config_params(CONFIGS[cfg])
+        plan = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"],
+                          sigma_r=p["sigma_r"], radius=p["radius"], n_terms=p["n_terms"],
+                          intensity_max=p["intensity_max"])
+        assert bfmod.launches(plan, 64, 64) == want, cfg
+    n = C.c_int(7)
+    assert L.bf_apply_launches(None, 4, 4, C.byref(n)) == bfmod.BF_ERR_INVALID_ARG
+    assert L.bf_apply_launches(plan.handle, 0, 4, C.byref(n)) == bfmod.BF_ERR_INVALID_ARG

@@ -64,7 +64,8 @@ def buckets(rep):
     rows = list(csv.reader(io.StringIO("\n".join(out.splitlines()[1:]))))
     h = rows[0]
     idx = {n: i for i, n in enumerate(h)}
-    g = collections.defaultdict(lambda: [0, 0, 0, collections.Counter()])
+    g = collections.defaultdict(lambda: [0, 0, 0, collections.Counter(), collections.Counter()])
+    stall_cols = [n for n in h if n.startswith("stall_") and "Not Issued" not in n]
     for r in rows[1:]:
         if len(r) < len(h):
             continue
@@ -77,10 +78,14 @@ def buckets(rep):
         e[1] += n
         e[2] += s
         e[3][op] += 1
+        for c in stall_cols:
+            e[4][c[6:]] += int(r[idx[c]] or 0)
     tot = sum(v[1] for v in g.values())
     print("\nexec-count  #instr  total-executed  share  samples  top opcodes")
-    for n, (ni, te, ss, ops) in sorted(g.items(), key=lambda kv: -kv[1][1])[:12]:
+    for n, (ni, te, ss, ops, st) in sorted(g.items(), key=lambda kv: -kv[1][2])[:12]:
         print(f"{n:>11,d} {ni:6d} {te:15,d} {100*te/tot:5.1f}% {ss:8d}  {dict(ops.most_common(6))}")
+        sst = sum(st.values()) or 1
+        print("              stalls: " + ", ".join(f"{k} {100*v/sst:.0f}%" for k, v in st.most_common(5)))
 
 
 if __name__ == "__main__" and len(sys.argv) > 1:
