@@ -200,45 +200,15 @@ struct Cheb64 {
 };
 
 
-// resident CTAs per SM the register budget is sized for
-template <int MAXK, int NT>
-struct Occ {
-  static constexpr int value = NT > 256 ? 1 : 2;
-};
+// ------------------------------------------------------------------ the four steps of a row
+// They are shared by the two kernels below (barrier-interval kernel, warp-specialised kernel).
 
-// FULL: nk == MAXK (no per-term runtime checks). CONSEC: the selected k are consecutive.
-template <int MAXK, int NB, bool U8, int NT, bool CONSEC, bool FULL>
-__global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
-    bf_band_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out,
-                   longlong2* __restrict__ ws) {
-  constexpr int UP = NT + 1;   // channel-row pitch (== 1 mod 32: lanes = channels are conflict-free)
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  int* Ubuf = reinterpret_cast<int*>(smem_raw);                               // [4 nk][UP]
-  float2* lut = reinterpret_cast<float2*>(smem_raw + P.l_off);                // [256]
-  double2* lut64 = reinterpret_cast<double2*>(lut + 256);                     // [256]
-
-  const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * P.TW;
-  const int y0 = blockIdx.y * P.TH;
-  const long long fbase = (long long)blockIdx.z * P.frame_elems;
-  const int col = x0 - P.rlo_x + tid;
-  const bool colok = (col >= 0) & (col < P.W);
-  const int TWv = min(P.TW, P.W - x0);
-  const int yend = min(y0 + P.TH, P.H);
+// Vertical state at row y0 - 1: U = urnd + sum over the rows v of the vertical boxes of the
+// quantised channels (every tap's scale carries the box weight, nested boxes add up).
+template <int MAXK, int NB, bool U8, bool CONSEC, bool FULL>
+__device__ __forceinline__ void v_init(const KParams& P, const void* __restrict__ in, const float2* lut,
+                                       long long fbase, int col, bool colok, int y0, int (&U)[4 * MAXK]) {
   const int nk = P.nk;
-
-  if (U8) {
-    for (int i = tid; i < 256; i += NT) {
-      double s, c;
-      sincospi((double)i * P.invD, &s, &c);
-      lut[i] = make_float2((float)c, (float)s);
-      lut64[i] = make_double2(c, s);
-    }
-    __syncthreads();
-  }
-
-  // ------------------------------------------------------------ vertical state at row y0 - 1
-  int U[4 * MAXK];
 #pragma unroll
   for (int ch = 0; ch < 4 * MAXK; ++ch) U[ch] = P.urnd;
   for (int v = P.vmin; v <= P.vmax; ++v) {
@@ -253,7 +223,6 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
     } else {
       base_angle_f32(I, P, c1, s1);
     }
-    float sc = 0.f, scI = 0.f;   // sum of the scales of the boxes that contain v (nested or not)
     float scb[NB], scIb[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
@@ -261,8 +230,6 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
       scb[b] = in_b ? P.qs[b] : 0.f;
       scIb[b] = in_b ? P.qsD[b] * I : 0.f;
     }
-    (void)sc;
-    (void)scI;
     float gc = 1.f, gs = 0.f;
     for (int j = 0; j < P.kstep[0]; ++j) rot1(gc, gs, c1, s1);
 #pragma unroll
@@ -283,209 +250,414 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
       }
     }
   }
+}
 
-  // tap rows of output row y, box b: enter y + vhi_b, leave y + vlo_b - 1
-  float Ipre[NB][2];
-  auto load_taps = [&](int y) {
+// input pixels of the taps of output row y, box b: enter y + vhi_b, leave y + vlo_b - 1
+template <int NB, bool U8>
+__device__ __forceinline__ void load_taps(const KParams& P, const void* __restrict__ in, long long fbase, int col,
+                                          bool colok, int y, float (&Ipre)[NB][2]) {
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int row = y + (j ? (P.vlo[b] - 1) : P.vhi[b]);
+      const bool ok = (b < P.nby) && colok && row >= 0 && row < P.H;
+      Ipre[b][j] = ok ? load_pixel(in, U8, fbase + (long long)row * P.W + col) : 0.f;
+    }
+  }
+}
+
+// V(y): slide the vertical state one row (enter / leave taps of every box, packed in pairs)
+// and store U' = U >> ush of every channel slot at Ucol[slot * UP].
+template <int MAXK, int NB, bool U8, bool CONSEC, bool FULL, int UP>
+__device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool colok, int y, const float (&Ipre)[NB][2],
+                                      int (&U)[4 * MAXK], int* Ucol) {
+  const int nk = P.nk;
+  u64 QS[NB], QI[NB];
+  Rot2 g2[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    float ce, se, cl, sl;
+    const float Ie = Ipre[b][0], Il = Ipre[b][1];
+    if (U8) {
+      const float2 te = lut[(int)Ie], tl = lut[(int)Il];
+      ce = te.x; se = te.y; cl = tl.x; sl = tl.y;
+    } else {
+      base_angle_f32(Ie, P, ce, se);
+      base_angle_f32(Il, P, cl, sl);
+    }
+    const int re = y + P.vhi[b], rl = y + P.vlo[b] - 1;
+    const bool oke = (b < P.nby) && colok && re >= 0 && re < P.H;
+    const bool okl = (b < P.nby) && colok && rl >= 0 && rl < P.H;
+    QS[b] = pk(oke ? P.qs[b] : 0.f, okl ? P.qs[b] : 0.f);
+    QI[b] = pk(oke ? P.qsD[b] * Ie : 0.f, okl ? P.qsD[b] * Il : 0.f);
+    g2[b].init(ce, se, cl, sl);
+    for (int j = 0; j < P.kstep[0]; ++j) g2[b].step();
+  }
+  const u64 MM = pk(MAGIC, MAGIC);
+#pragma unroll
+  for (int i = 0; i < MAXK; ++i) {
+    if (FULL || i < nk) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (i > 0) {
+          if (CONSEC) g2[b].step();
+          else
+            for (int j = 0; j < P.kstep[i]; ++j) g2[b].step();
+        }
+        const u64 C = g2[b].C, Sn = g2[b].S;
+        U[4 * i + 0] += diff_bits(fma2(C, QS[b], MM));
+        U[4 * i + 1] += diff_bits(fma2(Sn, QS[b], MM));
+        U[4 * i + 2] += diff_bits(fma2(C, QI[b], MM));
+        U[4 * i + 3] += diff_bits(fma2(Sn, QI[b], MM));
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) Ucol[(4 * i + t) * UP] = U[4 * i + t] >> P.ush;
+    }
+  }
+}
+
+// H(y) for one channel slot over output columns [xs, xe): slide the exact int32 horizontal box
+// sums H_b of U' and write F = (sum_b ax_b H_b + frnd) >> fsh (exact int64, narrowed) to
+// Fcol[x * FPX]. Ur[o + u] is U' at output column o, offset u.
+template <int NB, int FPX>
+__device__ __forceinline__ void walk_row(const KParams& P, const int* Ur, int* Fcol, int xs, int xe) {
+  int hlo[NB], hhi[NB], ax[NB];
+  int Hs[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    hlo[b] = P.hlo[b];
+    hhi[b] = P.hhi[b];
+    ax[b] = (b < P.nbx) ? P.ax[b] : 0;
+  }
+  // initial window sums at xs; a box nested in its successor's complement reuses the inner sum
+#pragma unroll
+  for (int b = NB - 1; b >= 0; --b) {
+    Hs[b] = 0;
+    if (b < P.nbx) {
+      int lo = xs + hlo[b], hi = xs + hhi[b];
+      int acc = 0, lo2 = hi + 1, hi2 = hi;
+      if (b + 1 < NB && b + 1 < P.nbx && hlo[b] <= hlo[b + 1] && hhi[b + 1] <= hhi[b]) {
+        acc = Hs[b + 1];
+        lo2 = xs + hhi[b + 1] + 1;
+        hi = xs + hlo[b + 1] - 1;
+      }
+      int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        int j = pass ? lo2 : lo;
+        const int je = pass ? hi2 : hi;
+        for (; j + 3 <= je; j += 4) {
+          a0 += Ur[j];
+          a1 += Ur[j + 1];
+          a2 += Ur[j + 2];
+          a3 += Ur[j + 3];
+        }
+        for (; j <= je; ++j) a0 += Ur[j];
+      }
+      Hs[b] = acc + (a0 + a1) + (a2 + a3);
+    }
+  }
+  const long long frnd = P.frnd;
+  const int fsh = P.fsh;
+  const int* pe[NB];
+  const int* pl[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    pe[b] = Ur + xs + 1 + hhi[b];
+    pl[b] = Ur + xs + hlo[b];
+  }
+  int* pf = Fcol + xs * FPX;
+  // software-pipelined: the taps of the next 4 outputs are loaded while these 4 are formed
+  // (reads past the segment end stay inside the shared-memory carve-up and are discarded)
+  int en[NB][4], ln[NB][4];
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      en[b][j] = pe[b][j];
+      ln[b][j] = pl[b][j];
+    }
+  int x = xs;
+  for (; x + 4 <= xe; x += 4) {
+    int e[NB][4], l[NB][4];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int row = y + (j ? (P.vlo[b] - 1) : P.vhi[b]);
-        const bool ok = (b < P.nby) && colok && row >= 0 && row < P.H;
-        Ipre[b][j] = ok ? load_pixel(in, U8, fbase + (long long)row * P.W + col) : 0.f;
+      for (int j = 0; j < 4; ++j) {
+        e[b][j] = en[b][j];
+        l[b][j] = ln[b][j];
+      }
+      pe[b] += 4;
+      pl[b] += 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        en[b][j] = pe[b][j];
+        ln[b][j] = pl[b][j];
       }
     }
-  };
-  load_taps(y0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      long long f = frnd;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) f += (long long)ax[b] * Hs[b];
+      pf[j * FPX] = (int)(f >> fsh);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) Hs[b] += e[b][j] - l[b][j];
+    }
+    pf += 4 * FPX;
+  }
+  for (int j = 0; x < xe; ++x, ++j) {   // tail (< 4 outputs): its taps are already in en / ln
+    long long f = frnd;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) f += (long long)ax[b] * Hs[b];
+    *pf = (int)(f >> fsh);
+    pf += FPX;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) Hs[b] += pe[b][j] - pl[b][j];
+  }
+}
+
+// C: num = sum_k W_c F_Ic + W_s F_Is, den = sum_k W_c F_c + W_s F_s for one output pixel with
+// the weights a_k cos / sin(k pi I(x) / D) in fp64 rounded to int32 (exact int64 sums); then
+// out = D num / den (den <= 0: out = I(x), Q18), or the int64 pair to the multi-pass workspace.
+template <int MAXK, bool U8, bool CONSEC, bool FULL>
+__device__ __forceinline__ void combine_pixel(const KParams& P, const double2* lut64, const int4* Fr, float Ic,
+                                              long long pix, float* __restrict__ out, longlong2* __restrict__ ws) {
+  const int nk = P.nk;
+  double c1, s1;
+  if (U8) {
+    const double2 t = lut64[(int)Ic];
+    c1 = t.x;
+    s1 = t.y;
+  } else {
+    base_angle_f64(Ic, P.invD, c1, s1);
+  }
+  Cheb64 g;
+  g.init(c1, s1);
+  for (int j = 0; j < P.kstep[0]; ++j) g.step();
+  long long num = 0, den = 0;
+#pragma unroll
+  for (int i = 0; i < MAXK; ++i) {
+    if (FULL || i < nk) {
+      if (i > 0) {
+        if (CONSEC) g.step();
+        else
+          for (int j = 0; j < P.kstep[i]; ++j) g.step();
+      }
+      const int wc = __double2loint(fma(g.c, P.aw[i], MAGIC64));
+      const int wsn = __double2loint(fma(g.s, P.aw[i], MAGIC64));
+      const int4 f = Fr[i];   // (F_c, F_s, F_Ic, F_Is) of term i
+      den += (long long)wc * f.x;
+      den += (long long)wsn * f.y;
+      num += (long long)wc * f.z;
+      num += (long long)wsn * f.w;
+    }
+  }
+  if (P.pass == 1) {
+    ws[pix] = make_longlong2(num, den);
+  } else {
+    if (P.pass >= 2) {
+      const longlong2 acc = ws[pix];
+      num += acc.x;
+      den += acc.y;
+    }
+    if (P.pass == 2) ws[pix] = make_longlong2(num, den);
+    else out[pix] = (den > 0) ? (float)(P.D * (double)num / (double)den) : Ic;
+  }
+}
+
+template <bool U8>
+__device__ __forceinline__ void fill_luts(const KParams& P, float2* lut, double2* lut64, int tid, int nthreads) {
+  if (U8) {
+    for (int i = tid; i < 256; i += nthreads) {
+      double s, c;
+      sincospi((double)i * P.invD, &s, &c);
+      lut[i] = make_float2((float)c, (float)s);
+      lut64[i] = make_double2(c, s);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ kernel 1: barrier intervals
+// One thread per extended column; per row interval A = V(y) + C(y-1), interval B = H(y).
+// Used for wide halos (NT = 512) and as the reference structure.
+template <int MAXK, int NT>
+struct Occ {
+  static constexpr int value = NT > 256 ? 1 : 2;
+};
+
+// FULL: nk == MAXK (no per-term runtime checks). CONSEC: the selected k are consecutive.
+template <int MAXK, int NB, bool U8, int NT, bool CONSEC, bool FULL>
+__global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
+    bf_band_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out,
+                   longlong2* __restrict__ ws) {
+  constexpr int UP = NT + 1;           // channel-row pitch (== 1 mod 32: lanes = channels are conflict-free)
+  constexpr int FPX = 4 * MAXK + 4;    // F pitch per output column (4 * odd: conflict-free int4 reads)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int* Ubuf = reinterpret_cast<int*>(smem_raw);                               // [4 nk][UP]
+  int* Fbuf = reinterpret_cast<int*>(smem_raw + P.f_off);                     // [TW][FPX]
+  float2* lut = reinterpret_cast<float2*>(smem_raw + P.l_off);                // [256]
+  double2* lut64 = reinterpret_cast<double2*>(lut + 256);                     // [256]
+
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * P.TW;
+  const int y0 = blockIdx.y * P.TH;
+  const long long fbase = (long long)blockIdx.z * P.frame_elems;
+  const int col = x0 - P.rlo_x + tid;
+  const bool colok = (col >= 0) & (col < P.W);
+  const int TWv = min(P.TW, P.W - x0);
+  const int yend = min(y0 + P.TH, P.H);
+
+  fill_luts<U8>(P, lut, lut64, tid, NT);
+  if (U8) __syncthreads();
+  int U[4 * MAXK];
+  v_init<MAXK, NB, U8, CONSEC, FULL>(P, in, lut, fbase, col, colok, y0, U);
+  float Ipre[NB][2];
+  load_taps<NB, U8>(P, in, fbase, col, colok, y0, Ipre);
 
   // walker of this thread (interval B): lane = channel slot, warp = (slot group, segment)
   const int wgrp = (tid >> 5) % P.ngrp;
   const int wseg = (tid >> 5) / P.ngrp;
   const int wslot = wgrp * 32 + (tid & 31);
-  const bool wact = (wslot < 4 * nk) && (wseg < P.nseg);
-  constexpr int FPX = 4 * MAXK + 4;   // F pitch per output column (4 * odd: conflict-free int4 reads)
-  int* Fbuf = reinterpret_cast<int*>(smem_raw + P.f_off);   // [TW][FPX]: F of output column x, channel slot
+  const bool wact = (wslot < 4 * P.nk) && (wseg < P.nseg);
   float Ic = 0.f;   // I(y - 1, x0 + tid) for the combine of row y - 1 (threads < TWv)
 
   for (int y = y0; y <= yend; ++y) {
     // ============================================================ interval A
     if (y < yend) {
-      // ---------------------------------------------------------- V(y): slide one row
-      u64 QS[NB], QI[NB];
-      Rot2 g2[NB];
+      float Icur[NB][2];
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
-        float ce, se, cl, sl;
-        const float Ie = Ipre[b][0], Il = Ipre[b][1];
-        if (U8) {
-          const float2 te = lut[(int)Ie], tl = lut[(int)Il];
-          ce = te.x; se = te.y; cl = tl.x; sl = tl.y;
-        } else {
-          base_angle_f32(Ie, P, ce, se);
-          base_angle_f32(Il, P, cl, sl);
-        }
-        const int re = y + P.vhi[b], rl = y + P.vlo[b] - 1;
-        const bool oke = (b < P.nby) && colok && re >= 0 && re < P.H;
-        const bool okl = (b < P.nby) && colok && rl >= 0 && rl < P.H;
-        QS[b] = pk(oke ? P.qs[b] : 0.f, okl ? P.qs[b] : 0.f);
-        QI[b] = pk(oke ? P.qsD[b] * Ie : 0.f, okl ? P.qsD[b] * Il : 0.f);
-        g2[b].init(ce, se, cl, sl);
-        for (int j = 0; j < P.kstep[0]; ++j) g2[b].step();
+        Icur[b][0] = Ipre[b][0];
+        Icur[b][1] = Ipre[b][1];
       }
-      if (y + 1 < yend) load_taps(y + 1);   // prefetch: lands during this row's work
-      const u64 MM = pk(MAGIC, MAGIC);
-#pragma unroll
-      for (int i = 0; i < MAXK; ++i) {
-        if (FULL || i < nk) {
-#pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            if (i > 0) {
-              if (CONSEC) g2[b].step();
-              else
-                for (int j = 0; j < P.kstep[i]; ++j) g2[b].step();
-            }
-            const u64 C = g2[b].C, Sn = g2[b].S;
-            U[4 * i + 0] += diff_bits(fma2(C, QS[b], MM));
-            U[4 * i + 1] += diff_bits(fma2(Sn, QS[b], MM));
-            U[4 * i + 2] += diff_bits(fma2(C, QI[b], MM));
-            U[4 * i + 3] += diff_bits(fma2(Sn, QI[b], MM));
-          }
-#pragma unroll
-          for (int t = 0; t < 4; ++t) Ubuf[(4 * i + t) * UP + tid] = U[4 * i + t] >> P.ush;
-        }
-      }
+      if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col, colok, y + 1, Ipre);   // prefetch
+      v_row<MAXK, NB, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + tid);
     }
-    // ------------------------------------------------------------ C(y-1): combine, normalise
-    // num = sum_k W_c F_Ic + W_s F_Is, den = sum_k W_c F_c + W_s F_s with the weights
-    // a_k cos / sin(k pi I(x) / D) computed in fp64 and rounded to integers (exact int64 sums).
-    if (y > y0 && tid < TWv) {
-      double c1, s1;
-      if (U8) {
-        const double2 t = lut64[(int)Ic];
-        c1 = t.x;
-        s1 = t.y;
-      } else {
-        base_angle_f64(Ic, P.invD, c1, s1);
-      }
-      Cheb64 g;
-      g.init(c1, s1);
-      for (int j = 0; j < P.kstep[0]; ++j) g.step();
-      long long num = 0, den = 0;
-      const int4* Fr = reinterpret_cast<const int4*>(Fbuf + tid * FPX);
-#pragma unroll
-      for (int i = 0; i < MAXK; ++i) {
-        if (FULL || i < nk) {
-          if (i > 0) {
-            if (CONSEC) g.step();
-            else
-              for (int j = 0; j < P.kstep[i]; ++j) g.step();
-          }
-          const int wc = __double2loint(fma(g.c, P.aw[i], MAGIC64));
-          const int wsn = __double2loint(fma(g.s, P.aw[i], MAGIC64));
-          const int4 f = Fr[i];   // (F_c, F_s, F_Ic, F_Is) of term i
-          den += (long long)wc * f.x;
-          den += (long long)wsn * f.y;
-          num += (long long)wc * f.z;
-          num += (long long)wsn * f.w;
-        }
-      }
-      const long long pix = fbase + (long long)(y - 1) * P.W + x0 + tid;
-      if (P.pass == 1) {
-        ws[pix] = make_longlong2(num, den);
-      } else {
-        if (P.pass >= 2) {
-          const longlong2 acc = ws[pix];
-          num += acc.x;
-          den += acc.y;
-        }
-        if (P.pass == 2) ws[pix] = make_longlong2(num, den);
-        else out[pix] = (den > 0) ? (float)(P.D * (double)num / (double)den) : Ic;
-      }
-    }
+    if (y > y0 && tid < TWv)
+      combine_pixel<MAXK, U8, CONSEC, FULL>(P, lut64, reinterpret_cast<const int4*>(Fbuf + tid * FPX), Ic,
+                                            fbase + (long long)(y - 1) * P.W + x0 + tid, out, ws);
     if (y >= yend) break;
     if (tid < TWv) Ic = load_pixel(in, U8, fbase + (long long)y * P.W + x0 + tid);
     __syncthreads();
-
     // ============================================================ interval B: H(y)
-    // Walkers slide the exact int32 horizontal box sums H_b of U' along the row and write
-    // F = (sum_b ax_b H_b + frnd) >> fsh (exact int64 product sum, narrowed). Lanes of a warp
-    // are 32 channels at the same x: conflict-free reads (pitch == 1 mod 32) and writes.
     if (wact) {
       const int xs = wseg * P.seglen;
       const int xe = min(xs + P.seglen, TWv);
-      if (xs < xe) {
-        const int* Ur = Ubuf + wslot * UP + P.rlo_x;   // Ur[o + u]: U' at output column o, offset u
-        int* Fr = Fbuf + wslot;   // Fr[x * FPX]
-        int hlo[NB], hhi[NB], ax[NB];
-        int Hs[NB];
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          hlo[b] = P.hlo[b];
-          hhi[b] = P.hhi[b];
-          ax[b] = (b < P.nbx) ? P.ax[b] : 0;
-        }
-        // initial window sums at xs; a box nested in its predecessor reuses the inner sum
-#pragma unroll
-        for (int b = NB - 1; b >= 0; --b) {
-          Hs[b] = 0;
-          if (b < P.nbx) {
-            int lo = xs + hlo[b], hi = xs + hhi[b];
-            int acc = 0, lo2 = hi + 1, hi2 = hi;
-            if (b + 1 < NB && b + 1 < P.nbx && hlo[b] <= hlo[b + 1] && hhi[b + 1] <= hhi[b]) {
-              acc = Hs[b + 1];
-              lo2 = xs + hhi[b + 1] + 1;
-              hi = xs + hlo[b + 1] - 1;
-            }
-            int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-#pragma unroll 1
-            for (int pass = 0; pass < 2; ++pass) {
-              int j = pass ? lo2 : lo;
-              const int je = pass ? hi2 : hi;
-              for (; j + 3 <= je; j += 4) {
-                a0 += Ur[j];
-                a1 += Ur[j + 1];
-                a2 += Ur[j + 2];
-                a3 += Ur[j + 3];
-              }
-              for (; j <= je; ++j) a0 += Ur[j];
-            }
-            Hs[b] = acc + (a0 + a1) + (a2 + a3);
-          }
-        }
-        const long long frnd = P.frnd;
-        const int fsh = P.fsh;
-        int x = xs;
-        for (; x + 4 <= xe; x += 4) {
-          int e[NB][4], l[NB][4];
-#pragma unroll
-          for (int b = 0; b < NB; ++b)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              e[b][j] = Ur[x + j + 1 + hhi[b]];
-              l[b][j] = Ur[x + j + hlo[b]];
-            }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            long long f = frnd;
-#pragma unroll
-            for (int b = 0; b < NB; ++b) f += (long long)ax[b] * Hs[b];
-            Fr[(x + j) * FPX] = (int)(f >> fsh);
-#pragma unroll
-            for (int b = 0; b < NB; ++b) Hs[b] += e[b][j] - l[b][j];
-          }
-        }
-        for (; x < xe; ++x) {
-          long long f = frnd;
-#pragma unroll
-          for (int b = 0; b < NB; ++b) f += (long long)ax[b] * Hs[b];
-          Fr[x * FPX] = (int)(f >> fsh);
-#pragma unroll
-          for (int b = 0; b < NB; ++b) Hs[b] += Ur[x + 1 + hhi[b]] - Ur[x + hlo[b]];
-        }
-      }
+      if (xs < xe) walk_row<NB, FPX>(P, Ubuf + wslot * UP + P.rlo_x, Fbuf + wslot, xs, xe);
     }
     __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ kernel 2: warp-specialised
+// Three warp roles connected by double-buffered shared-memory rows and named barriers, so the
+// vertical pass of row y+1 overlaps the horizontal pass of row y and the combine of row y-1:
+//   warps 0-7   V: one thread per extended column (NT = 256), producer of U'(y) rows
+//   warps 8-15  H: walkers, lane = channel slot, warp = (slot group, segment); U' -> F rows
+//   warps 16-19 C: combine / normalise / store, F -> output
+// Registers are redistributed with setmaxnreg (V 160, H 56, C 48 = 640 x 96).
+constexpr int WS_V = 256, WS_H = 256, WS_C = 128, WS_THREADS = WS_V + WS_H + WS_C;
+constexpr int BAR_U_FULL = 1, BAR_U_EMPTY = 3, BAR_F_FULL = 5, BAR_F_EMPTY = 7;   // + buffer index
+
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int MAXK, int NB, bool U8, bool CONSEC, bool FULL>
+__global__ void __launch_bounds__(WS_THREADS, 1)
+    bf_ws_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out, longlong2* __restrict__ ws) {
+  constexpr int NT = WS_V;
+  constexpr int UP = NT + 1;
+  constexpr int FPX = 4 * MAXK + 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ustride = 4 * P.nk * UP;                                          // ints per U' buffer
+  int* Ubuf = reinterpret_cast<int*>(smem_raw);                               // [2][4 nk][UP]
+  int* Fbuf = reinterpret_cast<int*>(smem_raw + P.f_off);                     // [2][TW][FPX]
+  const int fstride = P.TW * FPX;
+  float2* lut = reinterpret_cast<float2*>(smem_raw + P.l_off);
+  double2* lut64 = reinterpret_cast<double2*>(lut + 256);
+
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * P.TW;
+  const int y0 = blockIdx.y * P.TH;
+  const long long fbase = (long long)blockIdx.z * P.frame_elems;
+  const int TWv = min(P.TW, P.W - x0);
+  const int yend = min(y0 + P.TH, P.H);
+  constexpr int NUF = WS_V + WS_H;   // participants of the U' barriers
+  constexpr int NFF = WS_H + WS_C;   // participants of the F barriers
+
+  fill_luts<U8>(P, lut, lut64, tid, WS_THREADS);
+  __syncthreads();
+
+  if (tid < WS_V) {
+    // ------------------------------------------------------------ V role
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 160;");
+    const int col = x0 - P.rlo_x + tid;
+    const bool colok = (col >= 0) & (col < P.W);
+    int U[4 * MAXK];
+    v_init<MAXK, NB, U8, CONSEC, FULL>(P, in, lut, fbase, col, colok, y0, U);
+    float Ipre[NB][2];
+    load_taps<NB, U8>(P, in, fbase, col, colok, y0, Ipre);
+    for (int y = y0; y < yend; ++y) {
+      const int b = (y - y0) & 1;
+      float Icur[NB][2];
+#pragma unroll
+      for (int bb = 0; bb < NB; ++bb) {
+        Icur[bb][0] = Ipre[bb][0];
+        Icur[bb][1] = Ipre[bb][1];
+      }
+      if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col, colok, y + 1, Ipre);
+      if (y - y0 >= 2) bar_sync(BAR_U_EMPTY + b, NUF);
+      v_row<MAXK, NB, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + b * ustride + tid);
+      bar_arrive(BAR_U_FULL + b, NUF);
+    }
+    // drain: the walkers' last releases
+    for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_U_EMPTY + ((y - y0) & 1), NUF);
+  } else if (tid < WS_V + WS_H) {
+    // ------------------------------------------------------------ H role
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    const int ht = tid - WS_V;
+    const int wgrp = (ht >> 5) % P.ngrp;
+    const int wseg = (ht >> 5) / P.ngrp;
+    const int wslot = wgrp * 32 + (ht & 31);
+    const bool wact = (wslot < 4 * P.nk) && (wseg < P.nseg);
+    const int xs = wseg * P.seglen;
+    const int xe = min(xs + P.seglen, TWv);
+    for (int y = y0; y < yend; ++y) {
+      const int b = (y - y0) & 1;
+      bar_sync(BAR_U_FULL + b, NUF);
+      if (y - y0 >= 2) bar_sync(BAR_F_EMPTY + b, NFF);
+      if (wact && xs < xe)
+        walk_row<NB, FPX>(P, Ubuf + b * ustride + wslot * UP + P.rlo_x, Fbuf + b * fstride + wslot, xs, xe);
+      bar_arrive(BAR_U_EMPTY + b, NUF);
+      bar_arrive(BAR_F_FULL + b, NFF);
+    }
+    for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_F_EMPTY + ((y - y0) & 1), NFF);
+  } else {
+    // ------------------------------------------------------------ C role
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
+    const int ct = tid - WS_V - WS_H;
+    for (int y = y0; y < yend; ++y) {
+      const int b = (y - y0) & 1;
+      float Iv[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int o = ct + j * WS_C;
+        Iv[j] = (o < TWv) ? load_pixel(in, U8, fbase + (long long)y * P.W + x0 + o) : 0.f;
+      }
+      bar_sync(BAR_F_FULL + b, NFF);
+#pragma unroll 1
+      for (int j = 0; j < 2; ++j) {
+        const int o = ct + j * WS_C;
+        if (o < TWv)
+          combine_pixel<MAXK, U8, CONSEC, FULL>(P, lut64, reinterpret_cast<const int4*>(Fbuf + b * fstride + o * FPX),
+                                                Iv[j], fbase + (long long)y * P.W + x0 + o, out, ws);
+      }
+      bar_arrive(BAR_F_EMPTY + b, NFF);
+    }
   }
 }
 
@@ -511,8 +683,28 @@ size_t smem_layout(KParams& P, int NT, int MAXK, bool u8) {
   return off;
 }
 
+// warp-specialised kernel: two U' row buffers and two F row buffers
+size_t smem_layout_ws(KParams& P, int MAXK, bool u8) {
+  auto up16 = [](size_t v) { return (v + 15) / 16 * 16; };
+  size_t off = up16(sizeof(int) * 2 * 4 * (size_t)P.nk * (WS_V + 1));
+  P.f_off = (int)off;
+  off = up16(off + sizeof(int) * 2 * (size_t)P.TW * (4 * MAXK + 4));
+  P.l_off = (int)off;
+  if (u8) off += 256 * (sizeof(float2) + sizeof(double2));
+  return off;
+}
+
 template <int MAXK, int NB, bool U8, int NT, bool CONSEC, bool FULL = false>
-cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim3 grid, cudaStream_t st) {
+cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim3 grid, cudaStream_t st, bool wsk) {
+  if (NT == WS_V && wsk) {
+    auto kfn = bf_ws_kernel<MAXK, NB, U8, CONSEC, FULL>;
+    const size_t smem = smem_layout_ws(P, MAXK, U8);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, WS_THREADS, smem, st>>>(P, in, out, ws);
+    return cudaGetLastError();
+  }
   auto kfn = bf_band_kernel<MAXK, NB, U8, NT, CONSEC, FULL>;
   const size_t smem = smem_layout(P, NT, MAXK, U8);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
@@ -524,26 +716,33 @@ cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim
 
 template <int MAXK, bool U8, int NT>
 cudaError_t dispatch_nb(int nb, bool consec, const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool wsk) {
   const bool full = consec && P.nk == MAXK;
-  if (nb <= 1) return full ? launch_one<MAXK, 1, U8, NT, true, true>(P, in, out, ws, grid, st)
-                    : consec ? launch_one<MAXK, 1, U8, NT, true>(P, in, out, ws, grid, st)
-                             : launch_one<MAXK, 1, U8, NT, false>(P, in, out, ws, grid, st);
-  if (nb == 2) return full ? launch_one<MAXK, 2, U8, NT, true, true>(P, in, out, ws, grid, st)
-                    : consec ? launch_one<MAXK, 2, U8, NT, true>(P, in, out, ws, grid, st)
-                             : launch_one<MAXK, 2, U8, NT, false>(P, in, out, ws, grid, st);
-  return launch_one<MAXK, 4, U8, NT, false>(P, in, out, ws, grid, st);
+  if (nb <= 1) return full ? launch_one<MAXK, 1, U8, NT, true, true>(P, in, out, ws, grid, st, wsk)
+                    : consec ? launch_one<MAXK, 1, U8, NT, true>(P, in, out, ws, grid, st, wsk)
+                             : launch_one<MAXK, 1, U8, NT, false>(P, in, out, ws, grid, st, wsk);
+  if (nb == 2) return full ? launch_one<MAXK, 2, U8, NT, true, true>(P, in, out, ws, grid, st, wsk)
+                    : consec ? launch_one<MAXK, 2, U8, NT, true>(P, in, out, ws, grid, st, wsk)
+                             : launch_one<MAXK, 2, U8, NT, false>(P, in, out, ws, grid, st, wsk);
+  return launch_one<MAXK, 4, U8, NT, false>(P, in, out, ws, grid, st, false);
 }
 
 struct Shape {
   int NT, MAXK;
+  bool wsk;   // warp-specialised kernel (NT = 256, at most 2 boxes per axis)
 };
 
 // Thread-block shape per plan: NT extended columns (TW = NT - halo outputs, TW >= NT/2 where
 // possible) and MAXK terms per pass (the vertical state is 4*MAXK registers per thread).
-Shape choose_shape(int halo, int nk) {
-  Shape sh = halo <= 128 ? Shape{256, nk <= 8 ? 8 : 16} : Shape{512, 8};
+Shape choose_shape(int halo, int nk, int nb) {
+  // warp-specialised for NT = 256 except at 13-16 terms, where the barrier-interval kernel with
+  // two resident CTAs measured 2% faster on cfg2
+  Shape sh = halo <= 128 ? Shape{256, nk <= 8 ? 8 : 16, nb <= 2 && nk <= 12} : Shape{512, 8, false};
   if (const char* e = std::getenv("BF_MAXK")) sh.MAXK = std::atoi(e) <= 8 ? 8 : 16;   // tuning hook
+  if (const char* e = std::getenv("BF_KERNEL")) {   // tuning hook: force one kernel
+    if (std::strcmp(e, "band") == 0) sh.wsk = false;
+    if (std::strcmp(e, "ws") == 0) sh.wsk = (sh.NT == 256 && nb <= 2);
+  }
   if (sh.NT == 512) sh.MAXK = 8;
   return sh;
 }
@@ -551,9 +750,9 @@ Shape choose_shape(int halo, int nk) {
 template <bool U8>
 cudaError_t dispatch(const Shape& sh, int nb, bool consec, const KParams& P, const void* in, float* out,
                      longlong2* ws, dim3 grid, cudaStream_t st) {
-  if (sh.NT == 256 && sh.MAXK == 8) return dispatch_nb<8, U8, 256>(nb, consec, P, in, out, ws, grid, st);
-  if (sh.NT == 256 && sh.MAXK == 16) return dispatch_nb<16, U8, 256>(nb, consec, P, in, out, ws, grid, st);
-  if (sh.NT == 512 && sh.MAXK == 8) return dispatch_nb<8, U8, 512>(nb, consec, P, in, out, ws, grid, st);
+  if (sh.NT == 256 && sh.MAXK == 8) return dispatch_nb<8, U8, 256>(nb, consec, P, in, out, ws, grid, st, sh.wsk);
+  if (sh.NT == 256 && sh.MAXK == 16) return dispatch_nb<16, U8, 256>(nb, consec, P, in, out, ws, grid, st, sh.wsk);
+  if (sh.NT == 512 && sh.MAXK == 8) return dispatch_nb<8, U8, 512>(nb, consec, P, in, out, ws, grid, st, false);
   return cudaErrorInvalidConfiguration;
 }
 
@@ -569,9 +768,16 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
     rhi = std::max(rhi, p->hix[b]);
   }
   const int halo = rlo + rhi;
-  const Shape sh = choose_shape(halo, p->n_k);
+  Shape sh = choose_shape(halo, p->n_k, std::max(p->nbx, p->nby));
   if (halo + 32 > sh.NT) return BF_ERR_UNSUPPORTED;
   const int TW = sh.NT - halo;
+  if (sh.wsk) {   // the double-buffered rows must fit the 227 KB of shared memory
+    KParams Q;
+    std::memset(&Q, 0, sizeof(Q));
+    Q.TW = TW;
+    Q.nk = std::min(sh.MAXK, p->n_k);
+    if (smem_layout_ws(Q, sh.MAXK, p->input_dtype == BF_IN_U8) > 227 * 1024) sh.wsk = false;
+  }
   const int passes = (p->n_k + sh.MAXK - 1) / sh.MAXK;
   const int nstrips = (W + TW - 1) / TW;
 
@@ -639,7 +845,7 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
   // ---- band height: CTAs in whole waves of the resident slots, init (vmax - vmin + 1 rows)
   //      amortised over the band
   const int nsm = sm_count();
-  const int slots = nsm * (sh.NT > 256 ? 1 : 2);
+  const int slots = nsm * ((sh.NT > 256 || sh.wsk) ? 1 : 2);
   const int ry = P.vmax - P.vmin + 1;
   long long best_cost = -1;
   int best_nb = 1;
@@ -680,9 +886,9 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
     (void)prevk;
     // walker segments: ngrp * nseg warps <= NT / 32; long segments amortise the initial window
     // sums (2r+1 reads per box)
-    const int max_tasks = sh.NT / 32;
+    const int max_tasks = sh.wsk ? WS_H / 32 : sh.NT / 32;
     int nseg = std::max(1, max_tasks / P.ngrp);
-    const int min_len = std::max(32, 2 * (rlo + rhi + 1) / 3);
+    const int min_len = sh.wsk ? 24 : std::max(32, 2 * (rlo + rhi + 1) / 3);
     while (nseg > 1 && (TW + nseg - 1) / nseg < min_len) --nseg;
     if (const char* e = std::getenv("BF_NSEG")) nseg = std::max(1, std::min(max_tasks / P.ngrp, std::atoi(e)));  // tuning hook
     P.nseg = nseg;
@@ -721,7 +927,7 @@ extern "C" bf_status bf_apply_launches(const bf_plan* p, int H, int W, int* n) {
     rlo = std::max(rlo, -p->lox[b]);
     rhi = std::max(rhi, p->hix[b]);
   }
-  const Shape sh = choose_shape(rlo + rhi, p->n_k);
+  const Shape sh = choose_shape(rlo + rhi, p->n_k, std::max(p->nbx, p->nby));
   if (rlo + rhi + 32 > sh.NT) return BF_ERR_UNSUPPORTED;
   *n = (p->n_k + sh.MAXK - 1) / sh.MAXK;
   return BF_OK;

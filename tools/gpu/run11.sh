@@ -1,0 +1,4 @@
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for k in band ws; do for c in cfg2 cfg0 cfg1 cfg3; do BF_KERNEL=$k timeout 300 python bench.py --steps 10 --warmup 3 --config $c --no-cpu-baseline 2>&1 | tail -1 | cut -c170-230 | sed "s/^/$k $c /"; done; done
+BF_KERNEL=band BF_NSEG=3 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | cut -c170-230 | sed "s/^/band nseg3 /"
+BF_KERNEL=band BF_NSEG=4 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | cut -c170-230 | sed "s/^/band nseg4 /"

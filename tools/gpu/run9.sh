@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for k in band ws; do for c in cfg2 cfg0 cfg1 cfg3; do BF_KERNEL=$k timeout 300 python bench.py --steps 10 --warmup 3 --config $c --no-cpu-baseline 2>&1 | tail -1 | cut -c170-230 | sed "s/^/$k $c /"; done; done
+bash tools/gpu/prof.sh $1
