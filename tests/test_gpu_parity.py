@@ -179,3 +179,21 @@ def test_rank2_plan_is_rejected_loudly(gpu):
     img = torch.zeros((32, 32), dtype=torch.float32, device="cuda")
     with pytest.raises(pkg.BFError):
         pkg.bilateral_filter(gp, img)
+
+
+@pytest.mark.parametrize("cfg,H,W", [("cfg0", 256, 256), ("cfg1", 150, 347), ("cfg2", 333, 361), ("cfg3", 211, 333),
+                                     ("cfg1", 3, 500), ("cfg2", 97, 161)])
+def test_kernels_agree_bitwise(gpu, cfg, H, W, monkeypatch):
+    """The warp-specialised kernel (named-barrier pipeline, BF_KERNEL=ws) and the barrier-interval
+    kernel (BF_KERNEL=band) perform the same exact integer arithmetic with different schedules and
+    walker segmentations: their outputs must be bitwise equal (a synchronisation race would show)."""
+    pkg, torch = gpu
+    spec = CONFIGS[cfg]
+    img = config_input(spec, H=H, W=W)
+    gp, op = make_plans(pkg, config_params(spec), img.dtype)
+    outs = {}
+    for k in ("band", "ws"):
+        monkeypatch.setenv("BF_KERNEL", k)
+        outs[k] = run_gpu(pkg, torch, gp, img)
+    assert np.array_equal(outs["band"], outs["ws"])
+    assert_parity(outs["ws"], bf.bf_box(img, op), spec.intensity_max, cfg)
