@@ -119,6 +119,8 @@ typedef struct {
   int radius;                                /* spatial truncation radius r                    */
   double intensity_max;                      /* D                                              */
   int input_dtype;                           /* bf_input_dtype                                 */
+  int spatial_rank;                          /* terms fx_s(u) fy_s(v) of the GPU box-pair form:
+                                                1 separable, 2 rank-2 (e.g. N_s = 5), 0 none     */
 } bf_plan_info;
 
 /* Copies the plan contents into *info. */
@@ -134,7 +136,8 @@ BF_API bf_status bf_plan_get_info(const bf_plan* plan, bf_plan_info* info);
  * whose approximated denominator is <= 0 or not finite get out = I(x) (Q18). The result is
  * deterministic (fixed reduction order, exact integer box sums, no atomics).
  * Returns BF_ERR_INVALID_ARG for NULL pointers, H or W <= 0, H*W overflow or d_in == d_out;
- * BF_ERR_UNSUPPORTED if the plan's spatial factorisation is not separable.
+ * BF_ERR_UNSUPPORTED if the plan's spatial kernel has no box-pair form of rank <= 2 (see
+ * bf_plan_info.spatial_rank; rank 2 is K~_s = sum_{s<2} fx_s(u) fy_s(v) with box factors).
  */
 BF_API bf_status bf_apply(const bf_plan* plan, const void* d_in, float* d_out, int H, int W, bf_stream stream);
 

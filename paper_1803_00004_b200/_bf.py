@@ -45,6 +45,7 @@ class PlanInfo(C.Structure):
         ("box_lo_y", C.c_int * BF_MAX_AXIS_BOXES), ("box_hi_y", C.c_int * BF_MAX_AXIS_BOXES),
         ("box_w_y", C.c_double * BF_MAX_AXIS_BOXES),
         ("radius", C.c_int), ("intensity_max", C.c_double), ("input_dtype", C.c_int),
+        ("spatial_rank", C.c_int),
     ]
 
 
@@ -131,7 +132,7 @@ class Plan:
             separable=bool(inf.separable),
             boxes_x=[(inf.box_lo_x[i], inf.box_hi_x[i], inf.box_w_x[i]) for i in range(inf.nbx)],
             boxes_y=[(inf.box_lo_y[i], inf.box_hi_y[i], inf.box_w_y[i]) for i in range(inf.nby)],
-            radius=inf.radius, intensity_max=inf.intensity_max,
+            radius=inf.radius, intensity_max=inf.intensity_max, spatial_rank=inf.spatial_rank,
             input_dtype="u8" if inf.input_dtype == BF_IN_U8 else "f32")
 
     def close(self) -> None:

@@ -29,4 +29,12 @@ struct bf_plan {
   double wx[BF_MAX_AXIS_BOXES];
   int loy[BF_MAX_AXIS_BOXES], hiy[BF_MAX_AXIS_BOXES];
   double wy[BF_MAX_AXIS_BOXES];
+  // box-pair form for the GPU path (NEXT f3): K~_s(v, u) = sum_{s < ns} fx_s(u) fy_s(v), each
+  // factor a sum of boxes. ns = 1 is the separable plan above; ns = 2 covers the rank-2 plans
+  // (N_s = 5, the paper's three boxes), with fx_s = one nested elementary box each.
+  int ns;
+  int snbx[2], slox[2][BF_MAX_AXIS_BOXES], shix[2][BF_MAX_AXIS_BOXES];
+  double swx[2][BF_MAX_AXIS_BOXES];
+  int snby[2], sloy[2][BF_MAX_AXIS_BOXES], shiy[2][BF_MAX_AXIS_BOXES];
+  double swy[2][BF_MAX_AXIS_BOXES];
 };

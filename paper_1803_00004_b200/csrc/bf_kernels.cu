@@ -50,14 +50,16 @@ struct KParams {
   int H, W;
   long long frame_elems;
   int TW, TH, rlo_x;
-  int nbx, nby;
+  int ns;                     // box-pair terms: K~_s = sum_{s < ns} fx_s(u) fy_s(v) (1 = separable)
+  int nby;                    // vertical boxes (shared by the ns terms: one set of taps)
   int vlo[MAXB], vhi[MAXB];   // vertical boxes: row offsets (inclusive)
-  float qs[MAXB];             // their quantisation scales wy_b / max|wy| * 2^q (cos / sin channels)
-  float qsD[MAXB];            // qs_b / D (I cos / I sin channels)
+  float qs[2][MAXB];          // per term s: quantisation scales wy_sb / max|wy| * 2^q (cos / sin channels)
+  float qsD[2][MAXB];         // qs_sb / D (I cos / I sin channels)
   int vmin, vmax;             // union of the vertical boxes
   int urnd, ush;              // U' = (U + urnd) >> ush; urnd is folded into the initial state
-  int hlo[MAXB], hhi[MAXB];   // horizontal boxes: column offsets (inclusive)
-  int ax[MAXB];               // their integer weights round(wx_b / max|wx| * 2^27)
+  int nbx[2];                 // horizontal boxes of term s
+  int hlo[2][MAXB], hhi[2][MAXB];   // their column offsets (inclusive)
+  int ax[2][MAXB];            // their integer weights round(wx_sb / max|wx| * 2^27)
   int fsh;                    // F = (sum_b ax_b H_b + frnd) >> fsh fits int32
   long long frnd;
   int nk;                     // terms of this pass
@@ -200,17 +202,26 @@ struct Cheb64 {
 };
 
 
+// Spatial forms the kernels are instantiated for: NS box-pair terms, NBY vertical boxes (shared
+// taps), NBX horizontal boxes per term.
+template <int FORM>
+struct Form;
+template <> struct Form<1> { static constexpr int NS = 1, NBY = 1, NBX = 1; };   // one box (box K_s)
+template <> struct Form<2> { static constexpr int NS = 1, NBY = 2, NBX = 2; };   // separable, 2 nested boxes (N_s = 9)
+template <> struct Form<4> { static constexpr int NS = 1, NBY = 4, NBX = 4; };   // separable, up to 4 boxes
+template <> struct Form<5> { static constexpr int NS = 2, NBY = 2, NBX = 1; };   // rank 2 (N_s = 5, three boxes)
+
 // ------------------------------------------------------------------ the four steps of a row
 // They are shared by the two kernels below (barrier-interval kernel, warp-specialised kernel).
 
 // Vertical state at row y0 - 1: U = urnd + sum over the rows v of the vertical boxes of the
 // quantised channels (every tap's scale carries the box weight, nested boxes add up).
-template <int MAXK, int NB, bool U8, bool CONSEC, bool FULL>
+template <int MAXK, int NB, int NS, bool U8, bool CONSEC, bool FULL>
 __device__ __forceinline__ void v_init(const KParams& P, const void* __restrict__ in, const float2* lut,
-                                       long long fbase, int col, bool colok, int y0, int (&U)[4 * MAXK]) {
+                                       long long fbase, int col, bool colok, int y0, int (&U)[NS * 4 * MAXK]) {
   const int nk = P.nk;
 #pragma unroll
-  for (int ch = 0; ch < 4 * MAXK; ++ch) U[ch] = P.urnd;
+  for (int ch = 0; ch < NS * 4 * MAXK; ++ch) U[ch] = P.urnd;
   for (int v = P.vmin; v <= P.vmax; ++v) {
     const int row = y0 - 1 + v;
     const bool ok = colok && row >= 0 && row < P.H;
@@ -223,12 +234,15 @@ __device__ __forceinline__ void v_init(const KParams& P, const void* __restrict_
     } else {
       base_angle_f32(I, P, c1, s1);
     }
-    float scb[NB], scIb[NB];
+    float scb[NS][NB], scIb[NS][NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const bool in_b = ok && (b < P.nby) && v >= P.vlo[b] && v <= P.vhi[b];
-      scb[b] = in_b ? P.qs[b] : 0.f;
-      scIb[b] = in_b ? P.qsD[b] * I : 0.f;
+#pragma unroll
+      for (int t = 0; t < NS; ++t) {
+        scb[t][b] = in_b ? P.qs[t][b] : 0.f;
+        scIb[t][b] = in_b ? P.qsD[t][b] * I : 0.f;
+      }
     }
     float gc = 1.f, gs = 0.f;
     for (int j = 0; j < P.kstep[0]; ++j) rot1(gc, gs, c1, s1);
@@ -241,12 +255,15 @@ __device__ __forceinline__ void v_init(const KParams& P, const void* __restrict_
             for (int j = 0; j < P.kstep[i]; ++j) rot1(gc, gs, c1, s1);
         }
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          U[4 * i + 0] += quant(gc, scb[b]);
-          U[4 * i + 1] += quant(gs, scb[b]);
-          U[4 * i + 2] += quant(gc, scIb[b]);
-          U[4 * i + 3] += quant(gs, scIb[b]);
-        }
+        for (int t = 0; t < NS; ++t)
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            int* Ut = U + t * 4 * MAXK;
+            Ut[4 * i + 0] += quant(gc, scb[t][b]);
+            Ut[4 * i + 1] += quant(gs, scb[t][b]);
+            Ut[4 * i + 2] += quant(gc, scIb[t][b]);
+            Ut[4 * i + 3] += quant(gs, scIb[t][b]);
+          }
       }
     }
   }
@@ -269,11 +286,11 @@ __device__ __forceinline__ void load_taps(const KParams& P, const void* __restri
 
 // V(y): slide the vertical state one row (enter / leave taps of every box, packed in pairs)
 // and store U' = U >> ush of every channel slot at Ucol[slot * UP].
-template <int MAXK, int NB, bool U8, bool CONSEC, bool FULL, int UP>
+template <int MAXK, int NB, int NS, bool U8, bool CONSEC, bool FULL, int UP>
 __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool colok, int y, const float (&Ipre)[NB][2],
-                                      int (&U)[4 * MAXK], int* Ucol) {
+                                      int (&U)[NS * 4 * MAXK], int* Ucol) {
   const int nk = P.nk;
-  u64 QS[NB], QI[NB];
+  u64 QS[NS][NB], QI[NS][NB];
   Rot2 g2[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
@@ -289,8 +306,11 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
     const int re = y + P.vhi[b], rl = y + P.vlo[b] - 1;
     const bool oke = (b < P.nby) && colok && re >= 0 && re < P.H;
     const bool okl = (b < P.nby) && colok && rl >= 0 && rl < P.H;
-    QS[b] = pk(oke ? P.qs[b] : 0.f, okl ? P.qs[b] : 0.f);
-    QI[b] = pk(oke ? P.qsD[b] * Ie : 0.f, okl ? P.qsD[b] * Il : 0.f);
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      QS[t][b] = pk(oke ? P.qs[t][b] : 0.f, okl ? P.qs[t][b] : 0.f);
+      QI[t][b] = pk(oke ? P.qsD[t][b] * Ie : 0.f, okl ? P.qsD[t][b] * Il : 0.f);
+    }
     g2[b].init(ce, se, cl, sl);
     for (int j = 0; j < P.kstep[0]; ++j) g2[b].step();
   }
@@ -306,41 +326,57 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
             for (int j = 0; j < P.kstep[i]; ++j) g2[b].step();
         }
         const u64 C = g2[b].C, Sn = g2[b].S;
-        U[4 * i + 0] += diff_bits(fma2(C, QS[b], MM));
-        U[4 * i + 1] += diff_bits(fma2(Sn, QS[b], MM));
-        U[4 * i + 2] += diff_bits(fma2(C, QI[b], MM));
-        U[4 * i + 3] += diff_bits(fma2(Sn, QI[b], MM));
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+          int* Ut = U + t * 4 * MAXK;
+          Ut[4 * i + 0] += diff_bits(fma2(C, QS[t][b], MM));
+          Ut[4 * i + 1] += diff_bits(fma2(Sn, QS[t][b], MM));
+          Ut[4 * i + 2] += diff_bits(fma2(C, QI[t][b], MM));
+          Ut[4 * i + 3] += diff_bits(fma2(Sn, QI[t][b], MM));
+        }
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) Ucol[(4 * i + t) * UP] = U[4 * i + t] >> P.ush;
+      for (int t = 0; t < NS; ++t)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          Ucol[(t * 4 * nk + 4 * i + c) * UP] = U[t * 4 * MAXK + 4 * i + c] >> P.ush;
     }
   }
 }
 
 // H(y) for one channel slot over output columns [xs, xe): slide the exact int32 horizontal box
-// sums H_b of U' and write F = (sum_b ax_b H_b + frnd) >> fsh (exact int64, narrowed) to
-// Fcol[x * FPX]. Ur[o + u] is U' at output column o, offset u.
-template <int NB, int FPX>
-__device__ __forceinline__ void walk_row(const KParams& P, const int* Ur, int* Fcol, int xs, int xe) {
-  int hlo[NB], hhi[NB], ax[NB];
-  int Hs[NB];
+// sums H_tb of U'_t (term t, box b) and write F = (sum_tb ax_tb H_tb + frnd) >> fsh (exact int64,
+// narrowed) to Fcol[x * FPX]. Ur[o + u] is U'_0 at output column o, offset u; U'_t = Ur + t*srow.
+template <int NB, int NS, int FPX>
+__device__ __forceinline__ void walk_row(const KParams& P, const int* Ur, int srow, int* Fcol, int xs, int xe) {
+  constexpr int M = NS * NB;   // (term, box) streams
+  int hlo[M], hhi[M], ax[M];
+  int Hs[M];
+  const int* base[M];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    hlo[b] = P.hlo[b];
-    hhi[b] = P.hhi[b];
-    ax[b] = (b < P.nbx) ? P.ax[b] : 0;
-  }
-  // initial window sums at xs; a box nested in its successor's complement reuses the inner sum
+  for (int t = 0; t < NS; ++t)
 #pragma unroll
-  for (int b = NB - 1; b >= 0; --b) {
-    Hs[b] = 0;
-    if (b < P.nbx) {
-      int lo = xs + hlo[b], hi = xs + hhi[b];
+    for (int b = 0; b < NB; ++b) {
+      const int m = t * NB + b;
+      const bool on = b < P.nbx[t];
+      hlo[m] = on ? P.hlo[t][b] : 0;
+      hhi[m] = on ? P.hhi[t][b] : -1;   // empty box: no taps, H = 0
+      ax[m] = on ? P.ax[t][b] : 0;
+      base[m] = Ur + t * srow;
+    }
+  // initial window sums at xs; a box nested in the previous box of its term reuses the inner sum
+#pragma unroll
+  for (int t = 0; t < NS; ++t)
+#pragma unroll
+    for (int b = NB - 1; b >= 0; --b) {
+      const int m = t * NB + b;
+      const int* Urt = base[m];
+      int lo = xs + hlo[m], hi = xs + hhi[m];
       int acc = 0, lo2 = hi + 1, hi2 = hi;
-      if (b + 1 < NB && b + 1 < P.nbx && hlo[b] <= hlo[b + 1] && hhi[b + 1] <= hhi[b]) {
-        acc = Hs[b + 1];
-        lo2 = xs + hhi[b + 1] + 1;
-        hi = xs + hlo[b + 1] - 1;
+      if (b + 1 < NB && hhi[m + 1] >= hlo[m + 1] && hlo[m] <= hlo[m + 1] && hhi[m + 1] <= hhi[m]) {
+        acc = Hs[m + 1];
+        lo2 = xs + hhi[m + 1] + 1;
+        hi = xs + hlo[m + 1] - 1;
       }
       int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll 1
@@ -348,73 +384,72 @@ __device__ __forceinline__ void walk_row(const KParams& P, const int* Ur, int* F
         int j = pass ? lo2 : lo;
         const int je = pass ? hi2 : hi;
         for (; j + 3 <= je; j += 4) {
-          a0 += Ur[j];
-          a1 += Ur[j + 1];
-          a2 += Ur[j + 2];
-          a3 += Ur[j + 3];
+          a0 += Urt[j];
+          a1 += Urt[j + 1];
+          a2 += Urt[j + 2];
+          a3 += Urt[j + 3];
         }
-        for (; j <= je; ++j) a0 += Ur[j];
+        for (; j <= je; ++j) a0 += Urt[j];
       }
-      Hs[b] = acc + (a0 + a1) + (a2 + a3);
+      Hs[m] = acc + (a0 + a1) + (a2 + a3);
     }
-  }
   const long long frnd = P.frnd;
   const int fsh = P.fsh;
-  const int* pe[NB];
-  const int* pl[NB];
+  const int* pe[M];
+  const int* pl[M];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    pe[b] = Ur + xs + 1 + hhi[b];
-    pl[b] = Ur + xs + hlo[b];
+  for (int m = 0; m < M; ++m) {
+    pe[m] = base[m] + xs + 1 + hhi[m];
+    pl[m] = base[m] + xs + hlo[m];
   }
   int* pf = Fcol + xs * FPX;
   // software-pipelined: the taps of the next 4 outputs are loaded while these 4 are formed
   // (reads past the segment end stay inside the shared-memory carve-up and are discarded)
-  int en[NB][4], ln[NB][4];
+  int en[M][4], ln[M][4];
 #pragma unroll
-  for (int b = 0; b < NB; ++b)
+  for (int m = 0; m < M; ++m)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      en[b][j] = pe[b][j];
-      ln[b][j] = pl[b][j];
+      en[m][j] = pe[m][j];
+      ln[m][j] = pl[m][j];
     }
   int x = xs;
   for (; x + 4 <= xe; x += 4) {
-    int e[NB][4], l[NB][4];
+    int e[M][4], l[M][4];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
+    for (int m = 0; m < M; ++m) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        e[b][j] = en[b][j];
-        l[b][j] = ln[b][j];
+        e[m][j] = en[m][j];
+        l[m][j] = ln[m][j];
       }
-      pe[b] += 4;
-      pl[b] += 4;
+      pe[m] += 4;
+      pl[m] += 4;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        en[b][j] = pe[b][j];
-        ln[b][j] = pl[b][j];
+        en[m][j] = pe[m][j];
+        ln[m][j] = pl[m][j];
       }
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       long long f = frnd;
 #pragma unroll
-      for (int b = 0; b < NB; ++b) f += (long long)ax[b] * Hs[b];
+      for (int m = 0; m < M; ++m) f += (long long)ax[m] * Hs[m];
       pf[j * FPX] = (int)(f >> fsh);
 #pragma unroll
-      for (int b = 0; b < NB; ++b) Hs[b] += e[b][j] - l[b][j];
+      for (int m = 0; m < M; ++m) Hs[m] += e[m][j] - l[m][j];
     }
     pf += 4 * FPX;
   }
-  for (int j = 0; x < xe; ++x, ++j) {   // tail (< 4 outputs): its taps are already in en / ln
+  for (int j = 0; x < xe; ++x, ++j) {   // tail (< 4 outputs)
     long long f = frnd;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) f += (long long)ax[b] * Hs[b];
+    for (int m = 0; m < M; ++m) f += (long long)ax[m] * Hs[m];
     *pf = (int)(f >> fsh);
     pf += FPX;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) Hs[b] += pe[b][j] - pl[b][j];
+    for (int m = 0; m < M; ++m) Hs[m] += pe[m][j] - pl[m][j];
   }
 }
 
@@ -488,14 +523,15 @@ struct Occ {
 };
 
 // FULL: nk == MAXK (no per-term runtime checks). CONSEC: the selected k are consecutive.
-template <int MAXK, int NB, bool U8, int NT, bool CONSEC, bool FULL>
+template <int MAXK, int FORM, bool U8, int NT, bool CONSEC, bool FULL>
 __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
     bf_band_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out,
                    longlong2* __restrict__ ws) {
+  constexpr int NS = Form<FORM>::NS, NB = Form<FORM>::NBY, NBX = Form<FORM>::NBX;
   constexpr int UP = NT + 1;           // channel-row pitch (== 1 mod 32: lanes = channels are conflict-free)
   constexpr int FPX = 4 * MAXK + 4;    // F pitch per output column (4 * odd: conflict-free int4 reads)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int* Ubuf = reinterpret_cast<int*>(smem_raw);                               // [4 nk][UP]
+  int* Ubuf = reinterpret_cast<int*>(smem_raw);                               // [NS][4 nk][UP]
   int* Fbuf = reinterpret_cast<int*>(smem_raw + P.f_off);                     // [TW][FPX]
   float2* lut = reinterpret_cast<float2*>(smem_raw + P.l_off);                // [256]
   double2* lut64 = reinterpret_cast<double2*>(lut + 256);                     // [256]
@@ -511,8 +547,8 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
 
   fill_luts<U8>(P, lut, lut64, tid, NT);
   if (U8) __syncthreads();
-  int U[4 * MAXK];
-  v_init<MAXK, NB, U8, CONSEC, FULL>(P, in, lut, fbase, col, colok, y0, U);
+  int U[NS * 4 * MAXK];
+  v_init<MAXK, NB, NS, U8, CONSEC, FULL>(P, in, lut, fbase, col, colok, y0, U);
   float Ipre[NB][2];
   load_taps<NB, U8>(P, in, fbase, col, colok, y0, Ipre);
 
@@ -533,7 +569,7 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
         Icur[b][1] = Ipre[b][1];
       }
       if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col, colok, y + 1, Ipre);   // prefetch
-      v_row<MAXK, NB, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + tid);
+      v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + tid);
     }
     if (y > y0 && tid < TWv)
       combine_pixel<MAXK, U8, CONSEC, FULL>(P, lut64, reinterpret_cast<const int4*>(Fbuf + tid * FPX), Ic,
@@ -545,7 +581,7 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
     if (wact) {
       const int xs = wseg * P.seglen;
       const int xe = min(xs + P.seglen, TWv);
-      if (xs < xe) walk_row<NB, FPX>(P, Ubuf + wslot * UP + P.rlo_x, Fbuf + wslot, xs, xe);
+      if (xs < xe) walk_row<NBX, NS, FPX>(P, Ubuf + wslot * UP + P.rlo_x, 4 * P.nk * UP, Fbuf + wslot, xs, xe);
     }
     __syncthreads();
   }
@@ -557,7 +593,7 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
 //   warps 0-7   V: one thread per extended column (NT = 256), producer of U'(y) rows
 //   warps 8-15  H: walkers, lane = channel slot, warp = (slot group, segment); U' -> F rows
 //   warps 16-19 C: combine / normalise / store, F -> output
-// Registers are redistributed with setmaxnreg (V 160, H 56, C 48 = 640 x 96).
+// Registers are redistributed with setmaxnreg (V 152, H 56, C 56; 640 x 96 at launch).
 constexpr int WS_V = 256, WS_H = 256, WS_C = 128, WS_THREADS = WS_V + WS_H + WS_C;
 constexpr int BAR_U_FULL = 1, BAR_U_EMPTY = 3, BAR_F_FULL = 5, BAR_F_EMPTY = 7;   // + buffer index
 
@@ -566,15 +602,17 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int MAXK, int NB, bool U8, bool CONSEC, bool FULL>
+template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     bf_ws_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out, longlong2* __restrict__ ws) {
+  constexpr int NS = Form<FORM>::NS, NB = Form<FORM>::NBY, NBX = Form<FORM>::NBX;
   constexpr int NT = WS_V;
   constexpr int UP = NT + 1;
   constexpr int FPX = 4 * MAXK + 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int ustride = 4 * P.nk * UP;                                          // ints per U' buffer
-  int* Ubuf = reinterpret_cast<int*>(smem_raw);                               // [2][4 nk][UP]
+  const int srow = 4 * P.nk * UP;                                             // ints per term's U' rows
+  const int ustride = NS * srow;                                              // ints per U' buffer
+  int* Ubuf = reinterpret_cast<int*>(smem_raw);                               // [2][NS][4 nk][UP]
   int* Fbuf = reinterpret_cast<int*>(smem_raw + P.f_off);                     // [2][TW][FPX]
   const int fstride = P.TW * FPX;
   float2* lut = reinterpret_cast<float2*>(smem_raw + P.l_off);
@@ -594,11 +632,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 
   if (tid < WS_V) {
     // ------------------------------------------------------------ V role
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 160;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
     const int col = x0 - P.rlo_x + tid;
     const bool colok = (col >= 0) & (col < P.W);
-    int U[4 * MAXK];
-    v_init<MAXK, NB, U8, CONSEC, FULL>(P, in, lut, fbase, col, colok, y0, U);
+    int U[NS * 4 * MAXK];
+    v_init<MAXK, NB, NS, U8, CONSEC, FULL>(P, in, lut, fbase, col, colok, y0, U);
     float Ipre[NB][2];
     load_taps<NB, U8>(P, in, fbase, col, colok, y0, Ipre);
     for (int y = y0; y < yend; ++y) {
@@ -611,7 +649,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       }
       if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col, colok, y + 1, Ipre);
       if (y - y0 >= 2) bar_sync(BAR_U_EMPTY + b, NUF);
-      v_row<MAXK, NB, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + b * ustride + tid);
+      v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + b * ustride + tid);
       bar_arrive(BAR_U_FULL + b, NUF);
     }
     // drain: the walkers' last releases
@@ -631,14 +669,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       bar_sync(BAR_U_FULL + b, NUF);
       if (y - y0 >= 2) bar_sync(BAR_F_EMPTY + b, NFF);
       if (wact && xs < xe)
-        walk_row<NB, FPX>(P, Ubuf + b * ustride + wslot * UP + P.rlo_x, Fbuf + b * fstride + wslot, xs, xe);
+        walk_row<NBX, NS, FPX>(P, Ubuf + b * ustride + wslot * UP + P.rlo_x, srow, Fbuf + b * fstride + wslot, xs, xe);
       bar_arrive(BAR_U_EMPTY + b, NUF);
       bar_arrive(BAR_F_FULL + b, NFF);
     }
     for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_F_EMPTY + ((y - y0) & 1), NFF);
   } else {
     // ------------------------------------------------------------ C role
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     const int ct = tid - WS_V - WS_H;
     for (int y = y0; y < yend; ++y) {
       const int b = (y - y0) & 1;
@@ -675,7 +713,7 @@ int sm_count() {
 
 size_t smem_layout(KParams& P, int NT, int MAXK, bool u8) {
   auto up16 = [](size_t v) { return (v + 15) / 16 * 16; };
-  size_t off = up16(sizeof(int) * 4 * (size_t)P.nk * (NT + 1));
+  size_t off = up16(sizeof(int) * P.ns * 4 * (size_t)P.nk * (NT + 1));
   P.f_off = (int)off;
   off = up16(off + sizeof(int) * (size_t)P.TW * (4 * MAXK + 4));
   P.l_off = (int)off;
@@ -686,7 +724,7 @@ size_t smem_layout(KParams& P, int NT, int MAXK, bool u8) {
 // warp-specialised kernel: two U' row buffers and two F row buffers
 size_t smem_layout_ws(KParams& P, int MAXK, bool u8) {
   auto up16 = [](size_t v) { return (v + 15) / 16 * 16; };
-  size_t off = up16(sizeof(int) * 2 * 4 * (size_t)P.nk * (WS_V + 1));
+  size_t off = up16(sizeof(int) * 2 * P.ns * 4 * (size_t)P.nk * (WS_V + 1));
   P.f_off = (int)off;
   off = up16(off + sizeof(int) * 2 * (size_t)P.TW * (4 * MAXK + 4));
   P.l_off = (int)off;
@@ -694,18 +732,20 @@ size_t smem_layout_ws(KParams& P, int MAXK, bool u8) {
   return off;
 }
 
-template <int MAXK, int NB, bool U8, int NT, bool CONSEC, bool FULL = false>
+template <int MAXK, int FORM, bool U8, int NT, bool CONSEC, bool FULL = false>
 cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim3 grid, cudaStream_t st, bool wsk) {
-  if (NT == WS_V && wsk) {
-    auto kfn = bf_ws_kernel<MAXK, NB, U8, CONSEC, FULL>;
-    const size_t smem = smem_layout_ws(P, MAXK, U8);
-    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kfn<<<grid, WS_THREADS, smem, st>>>(P, in, out, ws);
-    return cudaGetLastError();
+  if constexpr (NT == WS_V && FORM != 4) {
+    if (wsk) {
+      auto kfn = bf_ws_kernel<MAXK, FORM, U8, CONSEC, FULL>;
+      const size_t smem = smem_layout_ws(P, MAXK, U8);
+      if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kfn<<<grid, WS_THREADS, smem, st>>>(P, in, out, ws);
+      return cudaGetLastError();
+    }
   }
-  auto kfn = bf_band_kernel<MAXK, NB, U8, NT, CONSEC, FULL>;
+  auto kfn = bf_band_kernel<MAXK, FORM, U8, NT, CONSEC, FULL>;
   const size_t smem = smem_layout(P, NT, MAXK, U8);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -714,45 +754,92 @@ cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim
   return cudaGetLastError();
 }
 
+template <int MAXK, int FORM, bool U8, int NT>
+cudaError_t dispatch_consec(bool consec, const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid,
+                            cudaStream_t st, bool wsk) {
+  if (consec && P.nk == MAXK) return launch_one<MAXK, FORM, U8, NT, true, true>(P, in, out, ws, grid, st, wsk);
+  if (consec) return launch_one<MAXK, FORM, U8, NT, true>(P, in, out, ws, grid, st, wsk);
+  return launch_one<MAXK, FORM, U8, NT, false>(P, in, out, ws, grid, st, wsk);
+}
+
 template <int MAXK, bool U8, int NT>
-cudaError_t dispatch_nb(int nb, bool consec, const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid,
-                        cudaStream_t st, bool wsk) {
-  const bool full = consec && P.nk == MAXK;
-  if (nb <= 1) return full ? launch_one<MAXK, 1, U8, NT, true, true>(P, in, out, ws, grid, st, wsk)
-                    : consec ? launch_one<MAXK, 1, U8, NT, true>(P, in, out, ws, grid, st, wsk)
-                             : launch_one<MAXK, 1, U8, NT, false>(P, in, out, ws, grid, st, wsk);
-  if (nb == 2) return full ? launch_one<MAXK, 2, U8, NT, true, true>(P, in, out, ws, grid, st, wsk)
-                    : consec ? launch_one<MAXK, 2, U8, NT, true>(P, in, out, ws, grid, st, wsk)
-                             : launch_one<MAXK, 2, U8, NT, false>(P, in, out, ws, grid, st, wsk);
-  return launch_one<MAXK, 4, U8, NT, false>(P, in, out, ws, grid, st, false);
+cudaError_t dispatch_form(int form, bool consec, const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid,
+                          cudaStream_t st, bool wsk) {
+  switch (form) {
+    case 1: return dispatch_consec<MAXK, 1, U8, NT>(consec, P, in, out, ws, grid, st, wsk);
+    case 2: return dispatch_consec<MAXK, 2, U8, NT>(consec, P, in, out, ws, grid, st, wsk);
+    case 4: return launch_one<MAXK, 4, U8, NT, false>(P, in, out, ws, grid, st, false);
+    default: break;
+  }
+  return cudaErrorInvalidConfiguration;
 }
 
 struct Shape {
   int NT, MAXK;
   bool wsk;   // warp-specialised kernel (NT = 256, at most 2 boxes per axis)
+  int form;   // Form<FORM>: 1, 2, 4 separable with that many boxes; 5 rank 2
 };
 
 // Thread-block shape per plan: NT extended columns (TW = NT - halo outputs, TW >= NT/2 where
-// possible) and MAXK terms per pass (the vertical state is 4*MAXK registers per thread).
-Shape choose_shape(int halo, int nk, int nb) {
+// possible), MAXK terms per pass (the vertical state is NS * 4 * MAXK registers per thread) and
+// the spatial form. Returns NT = 0 if the plan has no GPU form.
+Shape plan_shape(const bf_plan* p, int& rlo, int& rhi) {
+  Shape sh{0, 0, false, 0};
+  rlo = rhi = 0;
+  if (p->ns < 1 || p->ns > 2) return sh;
+  int nbx = 0, nby = p->snby[0];
+  for (int t = 0; t < p->ns; ++t) {
+    if (p->snbx[t] < 1 || p->snbx[t] > MAXB || p->snby[t] != nby) return sh;
+    nbx = std::max(nbx, p->snbx[t]);
+    for (int b = 0; b < p->snbx[t]; ++b) {
+      rlo = std::max(rlo, -p->slox[t][b]);
+      rhi = std::max(rhi, p->shix[t][b]);
+    }
+    for (int b = 0; b < nby; ++b)
+      if (p->sloy[t][b] != p->sloy[0][b] || p->shiy[t][b] != p->shiy[0][b]) return sh;
+  }
+  if (nby < 1 || nby > MAXB) return sh;
+  if (p->ns == 2) {
+    if (nbx > 1 || nby > 2) return sh;
+    sh.form = 5;
+  } else {
+    const int nb = std::max(nbx, nby);
+    sh.form = nb <= 1 ? 1 : (nb == 2 ? 2 : 4);
+  }
+  const int halo = rlo + rhi;
+  const int nk = p->n_k;
   // warp-specialised for NT = 256 except at 13-16 terms, where the barrier-interval kernel with
   // two resident CTAs measured 2% faster on cfg2
-  Shape sh = halo <= 128 ? Shape{256, nk <= 8 ? 8 : 16, nb <= 2 && nk <= 12} : Shape{512, 8, false};
-  if (const char* e = std::getenv("BF_MAXK")) sh.MAXK = std::atoi(e) <= 8 ? 8 : 16;   // tuning hook
+  if (halo <= 128) {
+    sh.NT = 256;
+    sh.MAXK = (nk <= 8 || p->ns == 2) ? 8 : 16;
+    sh.wsk = sh.form != 4 && (nk <= 12 || p->ns == 2);
+  } else {
+    sh.NT = 512;
+    sh.MAXK = 8;
+    sh.wsk = false;
+  }
+  if (const char* e = std::getenv("BF_MAXK")) sh.MAXK = (std::atoi(e) <= 8 || p->ns == 2) ? 8 : 16;   // tuning hook
   if (const char* e = std::getenv("BF_KERNEL")) {   // tuning hook: force one kernel
     if (std::strcmp(e, "band") == 0) sh.wsk = false;
-    if (std::strcmp(e, "ws") == 0) sh.wsk = (sh.NT == 256 && nb <= 2);
+    if (std::strcmp(e, "ws") == 0) sh.wsk = (sh.NT == 256 && sh.form != 4);
   }
   if (sh.NT == 512) sh.MAXK = 8;
+  if (halo + 32 > sh.NT) sh.NT = 0;
   return sh;
 }
 
 template <bool U8>
-cudaError_t dispatch(const Shape& sh, int nb, bool consec, const KParams& P, const void* in, float* out,
-                     longlong2* ws, dim3 grid, cudaStream_t st) {
-  if (sh.NT == 256 && sh.MAXK == 8) return dispatch_nb<8, U8, 256>(nb, consec, P, in, out, ws, grid, st, sh.wsk);
-  if (sh.NT == 256 && sh.MAXK == 16) return dispatch_nb<16, U8, 256>(nb, consec, P, in, out, ws, grid, st, sh.wsk);
-  if (sh.NT == 512 && sh.MAXK == 8) return dispatch_nb<8, U8, 512>(nb, consec, P, in, out, ws, grid, st, false);
+cudaError_t dispatch(const Shape& sh, bool consec, const KParams& P, const void* in, float* out, longlong2* ws,
+                     dim3 grid, cudaStream_t st) {
+  if (sh.form == 5) {   // rank 2: NS * 4 * 8 = 64 state registers, NT = 256 only
+    if (sh.NT != 256 || sh.MAXK != 8) return cudaErrorInvalidConfiguration;
+    return dispatch_consec<8, 5, U8, 256>(consec, P, in, out, ws, grid, st, sh.wsk);
+  }
+  if (sh.NT == 256 && sh.MAXK == 8) return dispatch_form<8, U8, 256>(sh.form, consec, P, in, out, ws, grid, st, sh.wsk);
+  if (sh.NT == 256 && sh.MAXK == 16)
+    return dispatch_form<16, U8, 256>(sh.form, consec, P, in, out, ws, grid, st, sh.wsk);
+  if (sh.NT == 512 && sh.MAXK == 8) return dispatch_form<8, U8, 512>(sh.form, consec, P, in, out, ws, grid, st, false);
   return cudaErrorInvalidConfiguration;
 }
 
@@ -761,25 +848,11 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
   if (!p || !d_in || !d_out || H <= 0 || W <= 0 || n_frames <= 0) return BF_ERR_INVALID_ARG;
   if ((long long)H * W > (1LL << 40) / n_frames) return BF_ERR_INVALID_ARG;
   if ((const void*)d_out == d_in) return BF_ERR_INVALID_ARG;
-  if (!p->separable || p->nbx > MAXB || p->nby > MAXB || p->nbx < 1 || p->nby < 1) return BF_ERR_UNSUPPORTED;
-  int rlo = 0, rhi = 0;
-  for (int b = 0; b < p->nbx; ++b) {
-    rlo = std::max(rlo, -p->lox[b]);
-    rhi = std::max(rhi, p->hix[b]);
-  }
-  const int halo = rlo + rhi;
-  Shape sh = choose_shape(halo, p->n_k, std::max(p->nbx, p->nby));
-  if (halo + 32 > sh.NT) return BF_ERR_UNSUPPORTED;
-  const int TW = sh.NT - halo;
-  if (sh.wsk) {   // the double-buffered rows must fit the 227 KB of shared memory
-    KParams Q;
-    std::memset(&Q, 0, sizeof(Q));
-    Q.TW = TW;
-    Q.nk = std::min(sh.MAXK, p->n_k);
-    if (smem_layout_ws(Q, sh.MAXK, p->input_dtype == BF_IN_U8) > 227 * 1024) sh.wsk = false;
-  }
-  const int passes = (p->n_k + sh.MAXK - 1) / sh.MAXK;
-  const int nstrips = (W + TW - 1) / TW;
+  int rlo, rhi;
+  Shape sh = plan_shape(p, rlo, rhi);
+  if (sh.NT == 0) return BF_ERR_UNSUPPORTED;
+  const int TW = sh.NT - (rlo + rhi);
+  const int ns = p->ns;
 
   KParams P;
   std::memset(&P, 0, sizeof(P));
@@ -788,41 +861,58 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
   P.frame_elems = (long long)H * W;
   P.TW = TW;
   P.rlo_x = rlo;
-  P.nbx = p->nbx;
-  P.nby = p->nby;
-  // ---- vertical: scales wy_b / max|wy| * 2^q, q as large as the int32 state allows
-  double wymax = 0.0, wsum = 0.0;
-  for (int b = 0; b < p->nby; ++b) wymax = std::max(wymax, std::fabs(p->wy[b]));
-  for (int b = 0; b < p->nby; ++b) wsum += std::fabs(p->wy[b]) / wymax * (p->hiy[b] - p->loy[b] + 1);
+  P.ns = ns;
+  P.nby = p->snby[0];
+  // ---- vertical: scales wy_tb / max|wy| * 2^q, q as large as the int32 states allow
+  double wymax = 0.0;
+  for (int t = 0; t < ns; ++t)
+    for (int b = 0; b < P.nby; ++b) wymax = std::max(wymax, std::fabs(p->swy[t][b]));
+  double wsum = 0.0;
+  for (int t = 0; t < ns; ++t) {
+    double w = 0.0;
+    for (int b = 0; b < P.nby; ++b) w += std::fabs(p->swy[t][b]) / wymax * (p->shiy[t][b] - p->sloy[t][b] + 1);
+    wsum = std::max(wsum, w);
+  }
   int qb = QBITS_MAX;
-  while (qb > 8 && std::ldexp(wsum, qb) + 4.0 * (p->hiy[0] - p->loy[0] + 8) >= 2147483647.0 - 65536.0) --qb;
-  double ubound = 0.0;   // bound of |U| before the shift
-  P.vmin = p->loy[0];
-  P.vmax = p->hiy[0];
-  for (int b = 0; b < p->nby; ++b) {
-    P.vlo[b] = p->loy[b];
-    P.vhi[b] = p->hiy[b];
-    P.qs[b] = (float)std::ldexp(p->wy[b] / wymax, qb);
-    P.qsD[b] = (float)((double)P.qs[b] / p->D);
-    ubound += (std::fabs((double)P.qs[b]) + 0.5) * (p->hiy[b] - p->loy[b] + 1);
-    P.vmin = std::min(P.vmin, p->loy[b]);
-    P.vmax = std::max(P.vmax, p->hiy[b]);
+  while (qb > 8 && std::ldexp(wsum, qb) + 4.0 * (p->shiy[0][0] - p->sloy[0][0] + 8) >= 2147483647.0 - 65536.0) --qb;
+  double ubound = 0.0;   // bound of |U_t| before the shift, over the terms
+  P.vmin = p->sloy[0][0];
+  P.vmax = p->shiy[0][0];
+  for (int b = 0; b < P.nby; ++b) {
+    P.vlo[b] = p->sloy[0][b];
+    P.vhi[b] = p->shiy[0][b];
+    P.vmin = std::min(P.vmin, P.vlo[b]);
+    P.vmax = std::max(P.vmax, P.vhi[b]);
+  }
+  for (int t = 0; t < ns; ++t) {
+    double ub = 0.0;
+    for (int b = 0; b < P.nby; ++b) {
+      P.qs[t][b] = (float)std::ldexp(p->swy[t][b] / wymax, qb);
+      P.qsD[t][b] = (float)((double)P.qs[t][b] / p->D);
+      ub += (std::fabs((double)P.qs[t][b]) + 0.5) * (P.vhi[b] - P.vlo[b] + 1);
+    }
+    ubound = std::max(ubound, ub);
   }
   int nxmax = 1;
-  for (int b = 0; b < p->nbx; ++b) nxmax = std::max(nxmax, p->hix[b] - p->lox[b] + 1);
+  for (int t = 0; t < ns; ++t)
+    for (int b = 0; b < p->snbx[t]; ++b) nxmax = std::max(nxmax, p->shix[t][b] - p->slox[t][b] + 1);
   P.ush = 0;
   while ((ubound / std::ldexp(1.0, P.ush) + 1.0) * nxmax >= 2147483000.0) ++P.ush;
   P.urnd = P.ush > 0 ? (1 << (P.ush - 1)) : 0;
   // ---- horizontal: integer weights, F narrowed to int32
   double wxmax = 0.0;
-  for (int b = 0; b < p->nbx; ++b) wxmax = std::max(wxmax, std::fabs(p->wx[b]));
+  for (int t = 0; t < ns; ++t)
+    for (int b = 0; b < p->snbx[t]; ++b) wxmax = std::max(wxmax, std::fabs(p->swx[t][b]));
   const double uprime = ubound / std::ldexp(1.0, P.ush) + 1.0;
   double fb = 0.0;
-  for (int b = 0; b < p->nbx; ++b) {
-    P.hlo[b] = p->lox[b];
-    P.hhi[b] = p->hix[b];
-    P.ax[b] = (int)std::lround(std::ldexp(p->wx[b] / wxmax, ABITS));
-    fb += std::fabs((double)P.ax[b]) * uprime * (p->hix[b] - p->lox[b] + 1);
+  for (int t = 0; t < ns; ++t) {
+    P.nbx[t] = p->snbx[t];
+    for (int b = 0; b < p->snbx[t]; ++b) {
+      P.hlo[t][b] = p->slox[t][b];
+      P.hhi[t][b] = p->shix[t][b];
+      P.ax[t][b] = (int)std::lround(std::ldexp(p->swx[t][b] / wxmax, ABITS));
+      fb += std::fabs((double)P.ax[t][b]) * uprime * (p->shix[t][b] - p->slox[t][b] + 1);
+    }
   }
   P.fsh = 0;
   while (fb / std::ldexp(1.0, P.fsh) >= 2147483000.0) ++P.fsh;
@@ -842,6 +932,13 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
   P.invD_lo = (float)(invD - (double)P.invD_hi);
   P.D = p->D;
 
+  const int passes = (p->n_k + sh.MAXK - 1) / sh.MAXK;
+  if (sh.wsk) {   // the double-buffered rows must fit the 227 KB of shared memory
+    KParams Q = P;
+    Q.nk = std::min(sh.MAXK, p->n_k);
+    if (smem_layout_ws(Q, sh.MAXK, p->input_dtype == BF_IN_U8) > 227 * 1024) sh.wsk = false;
+  }
+  const int nstrips = (W + TW - 1) / TW;
   // ---- band height: CTAs in whole waves of the resident slots, init (vmax - vmin + 1 rows)
   //      amortised over the band
   const int nsm = sm_count();
@@ -870,7 +967,6 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
   dim3 grid(nstrips, best_nb, n_frames);
   const bool u8 = (p->input_dtype == BF_IN_U8);
   cudaError_t err = cudaSuccess;
-  int prevk = 0;
   for (int pass = 0; pass < passes && err == cudaSuccess; ++pass) {
     const int first = pass * sh.MAXK;
     const int nk = std::min(sh.MAXK, p->n_k - first);
@@ -883,9 +979,7 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
       if (i > 0 && P.kstep[i] != 1) consec = false;
       P.aw[i] = std::ldexp(p->a[first + i], wbits);
     }
-    (void)prevk;
-    // walker segments: ngrp * nseg warps <= NT / 32; long segments amortise the initial window
-    // sums (2r+1 reads per box)
+    // walker segments: ngrp * nseg warps; long segments amortise the initial window sums
     const int max_tasks = sh.wsk ? WS_H / 32 : sh.NT / 32;
     int nseg = std::max(1, max_tasks / P.ngrp);
     const int min_len = sh.wsk ? 24 : std::max(32, 2 * (rlo + rhi + 1) / 3);
@@ -894,9 +988,8 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
     P.nseg = nseg;
     P.seglen = (TW + nseg - 1) / nseg;
     P.pass = (passes == 1) ? 0 : (pass == 0 ? 1 : (pass == passes - 1 ? 3 : 2));
-    const int nb = std::max(p->nbx, p->nby);
-    err = u8 ? dispatch<true>(sh, nb, consec, P, d_in, d_out, ws, grid, st)
-             : dispatch<false>(sh, nb, consec, P, d_in, d_out, ws, grid, st);
+    err = u8 ? dispatch<true>(sh, consec, P, d_in, d_out, ws, grid, st)
+             : dispatch<false>(sh, consec, P, d_in, d_out, ws, grid, st);
   }
   if (ws) cudaFreeAsync(ws, st);
   return err == cudaSuccess ? BF_OK : BF_ERR_CUDA;
@@ -921,14 +1014,9 @@ HostCache g_cache;
 extern "C" bf_status bf_apply_launches(const bf_plan* p, int H, int W, int* n) {
   if (!p || !n || H <= 0 || W <= 0) return BF_ERR_INVALID_ARG;
   *n = 0;
-  if (!p->separable || p->nbx > MAXB || p->nby > MAXB || p->nbx < 1 || p->nby < 1) return BF_ERR_UNSUPPORTED;
-  int rlo = 0, rhi = 0;
-  for (int b = 0; b < p->nbx; ++b) {
-    rlo = std::max(rlo, -p->lox[b]);
-    rhi = std::max(rhi, p->hix[b]);
-  }
-  const Shape sh = choose_shape(rlo + rhi, p->n_k, std::max(p->nbx, p->nby));
-  if (rlo + rhi + 32 > sh.NT) return BF_ERR_UNSUPPORTED;
+  int rlo, rhi;
+  const Shape sh = plan_shape(p, rlo, rhi);
+  if (sh.NT == 0) return BF_ERR_UNSUPPORTED;
   *n = (p->n_k + sh.MAXK - 1) / sh.MAXK;
   return BF_OK;
 }

@@ -232,6 +232,67 @@ bool step_to_boxes(const std::vector<double>& f, int r, int& nb, int lo[], int h
   return nb > 0;
 }
 
+// Rank-2 box-pair form of a symmetric lowered kernel K (n x n, [v][u]): the elementary nested
+// boxes of the x axis ([-e, e] at every edge of any row) and of the y axis, the weight matrix
+// W with K(v, u) = sum_ij W_ij [|u| <= e_i][|v| <= f_j] (2-D differences of K at the box
+// corners), then fx_s = [|u| <= e_s] and fy_s = sum_j W_sj [|v| <= f_j] for the (at most two)
+// x boxes. Returns false if K is not of that form (checked exactly on every offset).
+bool box_pair_rank2(const std::vector<double>& K, int r, bf_plan* p) {
+  const int n = 2 * r + 1;
+  double kmax = 0.0;
+  for (double v : K) kmax = std::max(kmax, std::fabs(v));
+  if (kmax == 0.0) return false;
+  const double tol = 1e-12 * kmax;
+  for (int v = 0; v < n; ++v)
+    for (int u = 0; u < n; ++u)
+      if (std::fabs(K[(size_t)v * n + u] - K[(size_t)(n - 1 - v) * n + (n - 1 - u)]) > tol ||
+          std::fabs(K[(size_t)v * n + u] - K[(size_t)v * n + (n - 1 - u)]) > tol)
+        return false;
+  // edges e (box [-e, e]) where some row / column changes value going outwards
+  std::vector<int> ex, ey;
+  for (int e = r; e >= 0; --e) {
+    bool cx = false, cy = false;
+    for (int t = 0; t < n; ++t) {
+      const double ox = (e == r) ? 0.0 : K[(size_t)t * n + (e + 1 + r)];   // value just outside, row t
+      const double oy = (e == r) ? 0.0 : K[(size_t)(e + 1 + r) * n + t];
+      if (std::fabs(K[(size_t)t * n + (e + r)] - ox) > tol) cx = true;
+      if (std::fabs(K[(size_t)(e + r) * n + t] - oy) > tol) cy = true;
+    }
+    if (cx) ex.push_back(e);
+    if (cy) ey.push_back(e);
+  }
+  const int nx = (int)ex.size(), ny = (int)ey.size();
+  if (nx < 1 || ny < 1 || nx > 2 || ny > BF_MAX_AXIS_BOXES) return false;
+  // M_ij = K(v = f_j, u = e_i) = sum_{i' <= i, j' <= j} W_i'j' (edges outermost first)
+  std::vector<double> W((size_t)nx * ny);
+  auto M = [&](int i, int j) { return (i < 0 || j < 0) ? 0.0 : K[(size_t)(ey[j] + r) * n + (ex[i] + r)]; };
+  for (int i = 0; i < nx; ++i)
+    for (int j = 0; j < ny; ++j) W[(size_t)i * ny + j] = M(i, j) - M(i - 1, j) - M(i, j - 1) + M(i - 1, j - 1);
+  for (int v = -r; v <= r; ++v)
+    for (int u = -r; u <= r; ++u) {
+      double k = 0.0;
+      for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < ny; ++j)
+          if (std::abs(u) <= ex[i] && std::abs(v) <= ey[j]) k += W[(size_t)i * ny + j];
+      if (std::fabs(k - K[(size_t)(v + r) * n + (u + r)]) > 1e-10 * kmax) return false;
+    }
+  p->ns = nx;
+  for (int s = 0; s < nx; ++s) {
+    p->snbx[s] = 1;
+    p->slox[s][0] = -ex[s];
+    p->shix[s][0] = ex[s];
+    p->swx[s][0] = 1.0;
+    p->snby[s] = 0;
+    for (int j = 0; j < ny; ++j) {
+      p->sloy[s][p->snby[s]] = -ey[j];
+      p->shiy[s][p->snby[s]] = ey[j];
+      p->swy[s][p->snby[s]] = W[(size_t)s * ny + j];   // zero weights kept: the states share taps
+      ++p->snby[s];
+    }
+  }
+  return true;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ public entry points
@@ -373,6 +434,24 @@ extern "C" bf_status bf_plan_create(bf_plan** out, int ks, int kr, double sigma_
       if (!okx || !oky) p->separable = 0;
     }
     if (!p->separable) p->nbx = p->nby = 0;
+    p->ns = 0;
+    if (p->separable) {
+      p->ns = 1;
+      p->snbx[0] = p->nbx;
+      p->snby[0] = p->nby;
+      for (int b = 0; b < p->nbx; ++b) {
+        p->slox[0][b] = p->lox[b];
+        p->shix[0][b] = p->hix[b];
+        p->swx[0][b] = p->wx[b];
+      }
+      for (int b = 0; b < p->nby; ++b) {
+        p->sloy[0][b] = p->loy[b];
+        p->shiy[0][b] = p->hiy[b];
+        p->swy[0][b] = p->wy[b];
+      }
+    } else if (!box_pair_rank2(K, radius, p)) {
+      p->ns = 0;   // no GPU form: bf_apply returns BF_ERR_UNSUPPORTED
+    }
   }
   *out = p;
   return BF_OK;
@@ -402,6 +481,7 @@ extern "C" bf_status bf_plan_get_info(const bf_plan* p, bf_plan_info* info) {
     info->sp_coef[i] = p->sp_coef[i];
   }
   info->separable = p->separable;
+  info->spatial_rank = p->ns;
   info->nbx = p->nbx;
   info->nby = p->nby;
   for (int i = 0; i < p->nbx; ++i) {

@@ -134,3 +134,15 @@ def test_launch_count_query(bfmod):
     n = C.c_int(7)
     assert L.bf_apply_launches(None, 4, 4, C.byref(n)) == bfmod.BF_ERR_INVALID_ARG
     assert L.bf_apply_launches(plan.handle, 0, 4, C.byref(n)) == bfmod.BF_ERR_INVALID_ARG
+
+
+def test_spatial_rank_of_the_gpu_form(bfmod):
+    """bf_plan_info.spatial_rank: 1 for the separable default plans (N_s = 9, box K_s), 2 for the
+    paper's three-box plan (N_s = 5); the rank-2 form's terms reproduce the lowered kernel."""
+    p = config_params(CONFIGS["cfg1"])
+    for ns, want in ((9, 1), (5, 2), (1, 1)):
+        plan = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"],
+                          sigma_r=p["sigma_r"], radius=p["radius"], n_terms=p["n_terms"], n_spatial=ns)
+        assert plan.info()["spatial_rank"] == want, ns
+    box = bfmod.Plan(spatial="box", range_kind="gaussian", sigma_s=1.0, sigma_r=15.0, radius=10, n_terms=4)
+    assert box.info()["spatial_rank"] == 1

@@ -173,12 +173,28 @@ def test_deterministic(gpu):
     assert np.array_equal(a, b)
 
 
-def test_rank2_plan_is_rejected_loudly(gpu):
+@pytest.mark.parametrize("cfg,H,W", [("cfg0", 150, 230), ("cfg1", 170, 260), ("cfg2", 140, 250)])
+def test_rank2_three_box_plan(gpu, cfg, H, W, monkeypatch):
+    """N_s = 5 (f1 + f2 + f3, the paper's three boxes): a rank-2 spatial kernel, run as two
+    box-pair terms (NEXT f3). Both kernels, against the oracle's box evaluation of the same plan."""
     pkg, torch = gpu
-    gp, _ = make_plans(pkg, config_params(CONFIGS["cfg0"]), np.float32, n_spatial=5)
-    img = torch.zeros((32, 32), dtype=torch.float32, device="cuda")
-    with pytest.raises(pkg.BFError):
-        pkg.bilateral_filter(gp, img)
+    spec = CONFIGS[cfg]
+    img = config_input(spec, H=H, W=W)
+    gp, op = make_plans(pkg, config_params(spec), img.dtype, n_spatial=5)
+    assert gp.info()["spatial_rank"] == 2 and not gp.info()["separable"]
+    ref, _, den, _ = bf.bf_box(img, op, return_parts=True)
+    # this kernel has negative corners: den can approach 0 (cfg1 has 4 pixels with den <= 0), where
+    # out = num / den is ill-conditioned and its fallback decision (den <= 0, Q18) flips on any
+    # rounding. Parity is asserted where den / sum(K~_s) >= 1e-3 (DESIGN.md reading Q26).
+    well = den / fit.spatial_kernel_values(op.sp).sum() >= 1e-3
+    assert well.mean() > 0.99
+    outs = []
+    for k in ("band", "ws"):
+        monkeypatch.setenv("BF_KERNEL", k)
+        outs.append(run_gpu(pkg, torch, gp, img))
+        assert np.all(np.isfinite(outs[-1]))
+        assert_parity(outs[-1][well], ref[well], spec.intensity_max, f"{cfg} N_s=5 {k}")
+    assert np.array_equal(outs[0], outs[1])
 
 
 @pytest.mark.parametrize("cfg,H,W", [("cfg0", 256, 256), ("cfg1", 150, 347), ("cfg2", 333, 361), ("cfg3", 211, 333),
