@@ -73,6 +73,8 @@ typedef struct {
 /* Maximum N (range terms) and N_s (spatial terms) accepted by bf_plan_create. */
 #define BF_MAX_TERMS 32
 #define BF_MAX_SPATIAL_TERMS 64
+/* Maximum range plans one bf_apply_multi evaluates over shared channels. */
+#define BF_MAX_PLANS 4
 /* Maximum boxes per axis of the separable spatial factor the GPU path runs. */
 #define BF_MAX_AXIS_BOXES 4
 
@@ -147,6 +149,19 @@ BF_API bf_status bf_apply(const bf_plan* plan, const void* d_in, float* d_out, i
  */
 BF_API bf_status bf_apply_batched(const bf_plan* plan, const void* d_in, float* d_out, int n_frames, int H, int W,
                            bf_stream stream);
+
+/*
+ * Case 1 of the paper's pre-computation: with T_{r_i} = D for every range kernel,
+ * the modulated channels F_c, F_s and their box sums do not depend on sigma_r, so n_plans range
+ * plans (e.g. several sigma_r, or Gaussian and Tukey) are evaluated in ONE pass that shares the
+ * vertical / horizontal box filtering; only the per-pixel combine runs per plan.
+ * plans[0..n_plans) must share the spatial plan (same boxes and weights), D and input dtype
+ * (else BF_ERR_INVALID_ARG); the union of their selected k must fit one pass (<= 16 terms, else
+ * BF_ERR_UNSUPPORTED). d_out holds n_plans H x W float32 images back to back (plan q at
+ * d_out + q*H*W). 1 <= n_plans <= BF_MAX_PLANS. Otherwise as bf_apply.
+ */
+BF_API bf_status bf_apply_multi(const bf_plan* const* plans, int n_plans, const void* d_in, float* d_out, int H, int W,
+                                bf_stream stream);
 
 /* Host-to-host convenience for end-to-end timing: copies h_in (host) to the device, filters,
  * copies the result back into h_out (host) and synchronises `stream`. Device buffers come

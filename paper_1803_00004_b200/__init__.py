@@ -10,10 +10,10 @@ streams; every step of the filter runs in the library's host fitter and sm_100a 
 """
 from __future__ import annotations
 
-from ._bf import (BFError, Plan, apply, apply_batched, apply_host, launches, lib, version)
+from ._bf import (BFError, Plan, apply, apply_batched, apply_host, apply_multi, launches, lib, version)
 
-__all__ = ["BFError", "Plan", "apply", "apply_batched", "apply_host", "bilateral_filter", "launches", "lib",
-           "version"]
+__all__ = ["BFError", "Plan", "apply", "apply_batched", "apply_host", "apply_multi", "bilateral_filter",
+           "bilateral_filter_multi", "launches", "lib", "version"]
 
 
 def _check_tensor(t, plan):
@@ -40,4 +40,18 @@ def bilateral_filter(plan: Plan, img, out=None, stream=None):
         apply_batched(plan, img.data_ptr(), out.data_ptr(), img.shape[0], img.shape[1], img.shape[2], s)
     else:
         raise ValueError("expected [H, W] or [F, H, W]")
+    return out
+
+
+def bilateral_filter_multi(plans, img, stream=None):
+    """Filters a [H, W] CUDA tensor with up to 4 range plans that share the spatial plan, in one
+    pass over shared box-filtered channels (Case 1 of P:1200-1219). Returns [len(plans), H, W]."""
+    import torch
+    for p in plans:
+        _check_tensor(img, p)
+    if img.dim() != 2:
+        raise ValueError("expected [H, W]")
+    out = torch.empty((len(plans),) + tuple(img.shape), dtype=torch.float32, device=img.device)
+    s = (stream or torch.cuda.current_stream(img.device)).cuda_stream
+    apply_multi(plans, img.data_ptr(), out.data_ptr(), img.shape[0], img.shape[1], s)
     return out

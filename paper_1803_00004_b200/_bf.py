@@ -23,7 +23,9 @@ RANGE = {"gaussian": BF_RANGE_GAUSSIAN, "tukey": BF_RANGE_TUKEY}
 
 #: every symbol include/bf.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bf_plan_options_default", "bf_plan_create", "bf_plan_destroy", "bf_plan_get_info", "bf_apply",
-           "bf_apply_batched", "bf_apply_host", "bf_apply_launches", "bf_status_string", "bf_version")
+           "bf_apply_batched", "bf_apply_host", "bf_apply_launches", "bf_apply_multi", "bf_status_string",
+           "bf_version")
+BF_MAX_PLANS = 4
 
 
 class PlanOptions(C.Structure):
@@ -81,6 +83,8 @@ def lib() -> C.CDLL:
         L.bf_apply_batched.restype = C.c_int
         L.bf_apply_host.argtypes = [P, P, P, C.c_int, C.c_int, P]
         L.bf_apply_host.restype = C.c_int
+        L.bf_apply_multi.argtypes = [C.POINTER(P), C.c_int, P, P, C.c_int, C.c_int, P]
+        L.bf_apply_multi.restype = C.c_int
         L.bf_apply_launches.argtypes = [P, C.c_int, C.c_int, C.POINTER(C.c_int)]
         L.bf_apply_launches.restype = C.c_int
         L.bf_status_string.argtypes = [C.c_int]
@@ -162,6 +166,14 @@ def apply_host(plan: Plan, h_in: int, h_out: int, H: int, W: int, stream: int = 
     """bf_apply_host on raw host pointers (copies in, filters, copies out, synchronises)."""
     _check(lib().bf_apply_host(plan.handle, C.c_void_p(h_in), C.c_void_p(h_out), int(H), int(W), C.c_void_p(stream)),
            "bf_apply_host")
+
+
+def apply_multi(plans, d_in: int, d_out: int, H: int, W: int, stream: int = 0) -> None:
+    """bf_apply_multi: several range plans over one pass of shared box-filtered channels (Case 1);
+    d_out holds len(plans) H x W float32 images back to back."""
+    arr = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
+    _check(lib().bf_apply_multi(arr, len(plans), C.c_void_p(d_in), C.c_void_p(d_out), int(H), int(W),
+                                C.c_void_p(stream)), "bf_apply_multi")
 
 
 def launches(plan: Plan, H: int, W: int) -> int:

@@ -45,6 +45,7 @@ constexpr double MAGIC64 = 6755399441055744.0;    // 1.5 * 2^52: low word of fma
 constexpr int QBITS_MAX = 22;                     // channel quantisation (the FFMA trick's range)
 constexpr int ABITS = 27;                         // horizontal integer box weights
 constexpr int MAXB = 4;                           // boxes per axis
+constexpr int MAXP = BF_MAX_PLANS;                // range plans of one bf_apply_multi
 
 struct KParams {
   int H, W;
@@ -64,7 +65,9 @@ struct KParams {
   long long frnd;
   int nk;                     // terms of this pass
   int kstep[BF_MAX_TERMS];    // Chebyshev steps before term i (term 0: from k = 0)
-  double aw[BF_MAX_TERMS];    // a_k * 2^wbits
+  double aw[BF_MAX_PLANS][16];   // a_k * 2^wbits of each range plan (bf_apply_multi; one plan otherwise)
+  int nplans;                 // range plans sharing the box-filtered channels (Case 1)
+  long long plan_stride;      // output elements between consecutive plans' images
   float invD_hi, invD_lo;     // 1/D as a float-float pair
   double invD, D;
   int pass;                   // 0 = only pass; 1 = first; 2 = middle; 3 = last
@@ -456,7 +459,7 @@ __device__ __forceinline__ void walk_row(const KParams& P, const int* Ur, int sr
 // C: num = sum_k W_c F_Ic + W_s F_Is, den = sum_k W_c F_c + W_s F_s for one output pixel with
 // the weights a_k cos / sin(k pi I(x) / D) in fp64 rounded to int32 (exact int64 sums); then
 // out = D num / den (den <= 0: out = I(x), Q18), or the int64 pair to the multi-pass workspace.
-template <int MAXK, bool U8, bool CONSEC, bool FULL>
+template <int MAXK, bool U8, bool CONSEC, bool FULL, bool MULTI>
 __device__ __forceinline__ void combine_pixel(const KParams& P, const double2* lut64, const int4* Fr, float Ic,
                                               long long pix, float* __restrict__ out, longlong2* __restrict__ ws) {
   const int nk = P.nk;
@@ -480,14 +483,45 @@ __device__ __forceinline__ void combine_pixel(const KParams& P, const double2* l
         else
           for (int j = 0; j < P.kstep[i]; ++j) g.step();
       }
-      const int wc = __double2loint(fma(g.c, P.aw[i], MAGIC64));
-      const int wsn = __double2loint(fma(g.s, P.aw[i], MAGIC64));
+      const int wc = __double2loint(fma(g.c, P.aw[0][i], MAGIC64));
+      const int wsn = __double2loint(fma(g.s, P.aw[0][i], MAGIC64));
       const int4 f = Fr[i];   // (F_c, F_s, F_Ic, F_Is) of term i
       den += (long long)wc * f.x;
       den += (long long)wsn * f.y;
       num += (long long)wc * f.z;
       num += (long long)wsn * f.w;
     }
+  }
+  if (MULTI) {   // bf_apply_multi: plans 1.. reuse the same F (single pass, no workspace)
+    out[pix] = (den > 0) ? (float)(P.D * (double)num / (double)den) : Ic;
+    g.init(c1, s1);
+    for (int j = 0; j < P.kstep[0]; ++j) g.step();
+    long long nu[MAXP - 1] = {}, de[MAXP - 1] = {};
+#pragma unroll
+    for (int i = 0; i < MAXK; ++i) {
+      if (FULL || i < nk) {
+        if (i > 0) {
+          if (CONSEC) g.step();
+          else
+            for (int j = 0; j < P.kstep[i]; ++j) g.step();
+        }
+        const int4 f = Fr[i];
+#pragma unroll
+        for (int q = 1; q < MAXP; ++q) {
+          if (q < P.nplans) {
+            const int wc = __double2loint(fma(g.c, P.aw[q][i], MAGIC64));
+            const int wsn = __double2loint(fma(g.s, P.aw[q][i], MAGIC64));
+            de[q - 1] += (long long)wc * f.x + (long long)wsn * f.y;
+            nu[q - 1] += (long long)wc * f.z + (long long)wsn * f.w;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 1; q < MAXP; ++q)
+      if (q < P.nplans)
+        out[pix + q * P.plan_stride] = (de[q - 1] > 0) ? (float)(P.D * (double)nu[q - 1] / (double)de[q - 1]) : Ic;
+    return;
   }
   if (P.pass == 1) {
     ws[pix] = make_longlong2(num, den);
@@ -523,7 +557,7 @@ struct Occ {
 };
 
 // FULL: nk == MAXK (no per-term runtime checks). CONSEC: the selected k are consecutive.
-template <int MAXK, int FORM, bool U8, int NT, bool CONSEC, bool FULL>
+template <int MAXK, int FORM, bool U8, int NT, bool CONSEC, bool FULL, bool MULTI>
 __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
     bf_band_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out,
                    longlong2* __restrict__ ws) {
@@ -572,7 +606,7 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
       v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + tid);
     }
     if (y > y0 && tid < TWv)
-      combine_pixel<MAXK, U8, CONSEC, FULL>(P, lut64, reinterpret_cast<const int4*>(Fbuf + tid * FPX), Ic,
+      combine_pixel<MAXK, U8, CONSEC, FULL, MULTI>(P, lut64, reinterpret_cast<const int4*>(Fbuf + tid * FPX), Ic,
                                             fbase + (long long)(y - 1) * P.W + x0 + tid, out, ws);
     if (y >= yend) break;
     if (tid < TWv) Ic = load_pixel(in, U8, fbase + (long long)y * P.W + x0 + tid);
@@ -602,7 +636,7 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL>
+template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL, bool MULTI>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     bf_ws_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out, longlong2* __restrict__ ws) {
   constexpr int NS = Form<FORM>::NS, NB = Form<FORM>::NBY, NBX = Form<FORM>::NBX;
@@ -691,7 +725,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       for (int j = 0; j < 2; ++j) {
         const int o = ct + j * WS_C;
         if (o < TWv)
-          combine_pixel<MAXK, U8, CONSEC, FULL>(P, lut64, reinterpret_cast<const int4*>(Fbuf + b * fstride + o * FPX),
+          combine_pixel<MAXK, U8, CONSEC, FULL, MULTI>(P, lut64, reinterpret_cast<const int4*>(Fbuf + b * fstride + o * FPX),
                                                 Iv[j], fbase + (long long)y * P.W + x0 + o, out, ws);
       }
       bar_arrive(BAR_F_EMPTY + b, NFF);
@@ -732,11 +766,11 @@ size_t smem_layout_ws(KParams& P, int MAXK, bool u8) {
   return off;
 }
 
-template <int MAXK, int FORM, bool U8, int NT, bool CONSEC, bool FULL = false>
+template <int MAXK, int FORM, bool U8, int NT, bool CONSEC, bool FULL = false, bool MULTI = false>
 cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim3 grid, cudaStream_t st, bool wsk) {
   if constexpr (NT == WS_V && FORM != 4) {
     if (wsk) {
-      auto kfn = bf_ws_kernel<MAXK, FORM, U8, CONSEC, FULL>;
+      auto kfn = bf_ws_kernel<MAXK, FORM, U8, CONSEC, FULL, MULTI>;
       const size_t smem = smem_layout_ws(P, MAXK, U8);
       if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
       cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -745,7 +779,7 @@ cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim
       return cudaGetLastError();
     }
   }
-  auto kfn = bf_band_kernel<MAXK, FORM, U8, NT, CONSEC, FULL>;
+  auto kfn = bf_band_kernel<MAXK, FORM, U8, NT, CONSEC, FULL, MULTI>;
   const size_t smem = smem_layout(P, NT, MAXK, U8);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -757,6 +791,13 @@ cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim
 template <int MAXK, int FORM, bool U8, int NT>
 cudaError_t dispatch_consec(bool consec, const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid,
                             cudaStream_t st, bool wsk) {
+  if (P.nplans > 1) {   // Case 1 multi-plan combine: its own instantiation (register pressure)
+    if constexpr (FORM == 1 || FORM == 2) {
+      return consec ? launch_one<MAXK, FORM, U8, NT, true, false, true>(P, in, out, ws, grid, st, wsk)
+                    : launch_one<MAXK, FORM, U8, NT, false, false, true>(P, in, out, ws, grid, st, wsk);
+    }
+    return cudaErrorInvalidConfiguration;
+  }
   if (consec && P.nk == MAXK) return launch_one<MAXK, FORM, U8, NT, true, true>(P, in, out, ws, grid, st, wsk);
   if (consec) return launch_one<MAXK, FORM, U8, NT, true>(P, in, out, ws, grid, st, wsk);
   return launch_one<MAXK, FORM, U8, NT, false>(P, in, out, ws, grid, st, wsk);
@@ -843,9 +884,46 @@ cudaError_t dispatch(const Shape& sh, bool consec, const KParams& P, const void*
   return cudaErrorInvalidConfiguration;
 }
 
-bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_frames, int H, int W,
-                     cudaStream_t st) {
-  if (!p || !d_in || !d_out || H <= 0 || W <= 0 || n_frames <= 0) return BF_ERR_INVALID_ARG;
+// Plans that can share one pass of box-filtered channels: same spatial form, D and input type.
+bool same_channels(const bf_plan* a, const bf_plan* b) {
+  if (a->ns != b->ns || a->D != b->D || a->input_dtype != b->input_dtype) return false;
+  for (int t = 0; t < a->ns; ++t) {
+    if (a->snbx[t] != b->snbx[t] || a->snby[t] != b->snby[t]) return false;
+    for (int i = 0; i < a->snbx[t]; ++i)
+      if (a->slox[t][i] != b->slox[t][i] || a->shix[t][i] != b->shix[t][i] || a->swx[t][i] != b->swx[t][i])
+        return false;
+    for (int i = 0; i < a->snby[t]; ++i)
+      if (a->sloy[t][i] != b->sloy[t][i] || a->shiy[t][i] != b->shiy[t][i] || a->swy[t][i] != b->swy[t][i])
+        return false;
+  }
+  return true;
+}
+
+bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, float* d_out, int n_frames, int H,
+                     int W, cudaStream_t st) {
+  if (!plans || nplans < 1 || nplans > MAXP || !d_in || !d_out || H <= 0 || W <= 0 || n_frames <= 0)
+    return BF_ERR_INVALID_ARG;
+  for (int q = 0; q < nplans; ++q)
+    if (!plans[q]) return BF_ERR_INVALID_ARG;
+  // union of the plans' selected k (one set of channels); a single plan is its own union
+  bf_plan merged = *plans[0];
+  if (nplans > 1) {
+    if (n_frames != 1) return BF_ERR_INVALID_ARG;
+    int ks[BF_MAX_TERMS * MAXP], nks = 0;
+    for (int q = 0; q < nplans; ++q) {
+      if (!same_channels(plans[0], plans[q])) return BF_ERR_INVALID_ARG;
+      for (int i = 0; i < plans[q]->n_k; ++i) ks[nks++] = plans[q]->k[i];
+    }
+    std::sort(ks, ks + nks);
+    nks = (int)(std::unique(ks, ks + nks) - ks);
+    if (nks > 16) return BF_ERR_UNSUPPORTED;
+    merged.n_k = nks;
+    for (int i = 0; i < nks; ++i) {
+      merged.k[i] = ks[i];
+      merged.a[i] = 0.0;
+    }
+  }
+  const bf_plan* p = &merged;
   if ((long long)H * W > (1LL << 40) / n_frames) return BF_ERR_INVALID_ARG;
   if ((const void*)d_out == d_in) return BF_ERR_INVALID_ARG;
   int rlo, rhi;
@@ -919,9 +997,13 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
   P.frnd = P.fsh > 0 ? (1LL << (P.fsh - 1)) : 0;
   // ---- combine weights a_k * 2^wbits: |W| < 2^31 and |num|, |den| < 2^62
   double asum = 0.0, amax = 0.0;
-  for (int i = 0; i < p->n_k; ++i) {
-    asum += std::fabs(p->a[i]);
-    amax = std::max(amax, std::fabs(p->a[i]));
+  for (int q = 0; q < nplans; ++q) {
+    double s1 = 0.0;
+    for (int i = 0; i < plans[q]->n_k; ++i) {
+      s1 += std::fabs(plans[q]->a[i]);
+      amax = std::max(amax, std::fabs(plans[q]->a[i]));
+    }
+    asum = std::max(asum, s1);
   }
   int wbits = 29;
   while (wbits > 8 && (std::ldexp(asum, wbits) * 2.0 * 2147483648.0 >= 4.0e18 || std::ldexp(amax, wbits) >= 2.0e9))
@@ -933,6 +1015,9 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
   P.D = p->D;
 
   const int passes = (p->n_k + sh.MAXK - 1) / sh.MAXK;
+  if (nplans > 1 && passes > 1) return BF_ERR_UNSUPPORTED;   // shared channels must fit one pass
+  P.nplans = nplans;
+  P.plan_stride = (long long)H * W;
   if (sh.wsk) {   // the double-buffered rows must fit the 227 KB of shared memory
     KParams Q = P;
     Q.nk = std::min(sh.MAXK, p->n_k);
@@ -977,7 +1062,16 @@ bf_status run_filter(const bf_plan* p, const void* d_in, float* d_out, int n_fra
       const int kk = p->k[first + i];
       P.kstep[i] = (i == 0) ? kk : kk - p->k[first + i - 1];
       if (i > 0 && P.kstep[i] != 1) consec = false;
-      P.aw[i] = std::ldexp(p->a[first + i], wbits);
+      if (nplans == 1) {
+        P.aw[0][i] = std::ldexp(p->a[first + i], wbits);
+      } else {
+        for (int q = 0; q < nplans; ++q) {   // a_k of plan q, 0 where q did not select k
+          double a = 0.0;
+          for (int j = 0; j < plans[q]->n_k; ++j)
+            if (plans[q]->k[j] == kk) a = plans[q]->a[j];
+          P.aw[q][i] = std::ldexp(a, wbits);
+        }
+      }
     }
     // walker segments: ngrp * nseg warps; long segments amortise the initial window sums
     const int max_tasks = sh.wsk ? WS_H / 32 : sh.NT / 32;
@@ -1022,12 +1116,17 @@ extern "C" bf_status bf_apply_launches(const bf_plan* p, int H, int W, int* n) {
 }
 
 extern "C" bf_status bf_apply(const bf_plan* plan, const void* d_in, float* d_out, int H, int W, bf_stream stream) {
-  return run_filter(plan, d_in, d_out, 1, H, W, reinterpret_cast<cudaStream_t>(stream));
+  return run_filter(&plan, 1, d_in, d_out, 1, H, W, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" bf_status bf_apply_multi(const bf_plan* const* plans, int n_plans, const void* d_in, float* d_out, int H,
+                                    int W, bf_stream stream) {
+  return run_filter(plans, n_plans, d_in, d_out, 1, H, W, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" bf_status bf_apply_batched(const bf_plan* plan, const void* d_in, float* d_out, int n_frames, int H,
                                       int W, bf_stream stream) {
-  return run_filter(plan, d_in, d_out, n_frames, H, W, reinterpret_cast<cudaStream_t>(stream));
+  return run_filter(&plan, 1, d_in, d_out, n_frames, H, W, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float* h_out, int H, int W,
@@ -1050,7 +1149,7 @@ extern "C" bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float*
     g_cache.out_bytes = ob;
   }
   if (cudaMemcpyAsync(g_cache.din, h_in, ib, cudaMemcpyHostToDevice, st) != cudaSuccess) return BF_ERR_CUDA;
-  bf_status s = run_filter(plan, g_cache.din, g_cache.dout, 1, H, W, st);
+  bf_status s = run_filter(&plan, 1, g_cache.din, g_cache.dout, 1, H, W, st);
   if (s != BF_OK) return s;
   if (cudaMemcpyAsync(h_out, g_cache.dout, ob, cudaMemcpyDeviceToHost, st) != cudaSuccess) return BF_ERR_CUDA;
   if (cudaStreamSynchronize(st) != cudaSuccess) return BF_ERR_CUDA;

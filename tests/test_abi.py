@@ -30,7 +30,7 @@ def header_functions():
 def test_header_declares_expected_api():
     assert header_functions() == sorted(["bf_plan_options_default", "bf_plan_create", "bf_plan_destroy",
                                          "bf_plan_get_info", "bf_apply", "bf_apply_batched", "bf_apply_host",
-                                         "bf_apply_launches", "bf_status_string", "bf_version"])
+                                         "bf_apply_launches", "bf_apply_multi", "bf_status_string", "bf_version"])
 
 
 def test_library_exports_every_declared_symbol(bfmod):

@@ -213,3 +213,28 @@ def test_kernels_agree_bitwise(gpu, cfg, H, W, monkeypatch):
         outs[k] = run_gpu(pkg, torch, gp, img)
     assert np.array_equal(outs["band"], outs["ws"])
     assert_parity(outs["ws"], bf.bf_box(img, op), spec.intensity_max, cfg)
+
+
+def test_multi_plan_case1_shared_channels(gpu):
+    """bf_apply_multi (Case 1 of P:1200-1219): several range kernels over one pass of shared
+    box-filtered channels. Each plan's image matches the oracle of that plan (and the plan's own
+    bf_apply within the tolerance: the combine weights are scaled for the set, not bitwise)."""
+    pkg, torch = gpu
+    spec = CONFIGS["cfg1"]
+    img = config_input(spec, H=150, W=233)
+    base = config_params(spec)
+    variants = [dict(sigma_r=10.0), dict(sigma_r=20.0), dict(sigma_r=45.0), dict(range_kind="tukey", sigma_r=40.0)]
+    plans, refs = [], []
+    for v in variants:
+        gp, op = make_plans(pkg, base, img.dtype, **v)
+        plans.append(gp)
+        refs.append(bf.bf_box(img, op))
+    t = torch.from_numpy(img).cuda()
+    outs = pkg.bilateral_filter_multi(plans, t).cpu().numpy().astype(np.float64)
+    for q, (gp, ref) in enumerate(zip(plans, refs)):
+        assert_parity(outs[q], ref, 255.0, f"plan {q}")
+        assert_parity(outs[q], run_gpu(pkg, torch, gp, img), 255.0, f"plan {q} vs bf_apply")
+    # plans must share the spatial plan
+    other, _ = make_plans(pkg, base, img.dtype, sigma_s=5.0)
+    with pytest.raises(pkg.BFError):
+        pkg.bilateral_filter_multi([plans[0], other], t)
