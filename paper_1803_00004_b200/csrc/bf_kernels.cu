@@ -160,6 +160,31 @@ __device__ __forceinline__ u64 mul2(u64 a, u64 b) {
   return r;
 }
 
+// base_angle_f32 on a packed pair of inputs (FFMA2 / FMUL2), bit-identical per lane: the sine
+// polynomial runs with negated coefficients so that its product with t' is -p t' directly.
+__device__ __forceinline__ void base_angle_f32x2(float Ia, float Ib, const KParams& P, u64& C1, u64& S1) {
+  const u64 I2 = pk(Ia, Ib);
+  u64 t = fma2(I2, pk(P.invD_hi, P.invD_hi), pk(-0.5f, -0.5f));
+  t = fma2(I2, pk(P.invD_lo, P.invD_lo), t);
+  const u64 z = mul2(t, t);
+  u64 p = pk(7.022163365e-03f, 7.022163365e-03f);
+  p = fma2(p, z, pk(-8.204647899e-02f, -8.204647899e-02f));
+  p = fma2(p, z, pk(5.992513299e-01f, 5.992513299e-01f));
+  p = fma2(p, z, pk(-2.550163269e+00f, -2.550163269e+00f));
+  p = fma2(p, z, pk(5.167712688e+00f, 5.167712688e+00f));
+  p = fma2(p, z, pk(-3.141592741e+00f, -3.141592741e+00f));
+  u64 q = pk(-1.004332444e-04f, -1.004332444e-04f);
+  q = fma2(q, z, pk(1.927883714e-03f, 1.927883714e-03f));
+  q = fma2(q, z, pk(-2.580653690e-02f, -2.580653690e-02f));
+  q = fma2(q, z, pk(2.353305817e-01f, 2.353305817e-01f));
+  q = fma2(q, z, pk(-1.335262775e+00f, -1.335262775e+00f));
+  q = fma2(q, z, pk(4.058712006e+00f, 4.058712006e+00f));
+  q = fma2(q, z, pk(-4.934802055e+00f, -4.934802055e+00f));
+  q = fma2(q, z, pk(1.0f, 1.0f));
+  C1 = mul2(p, t);
+  S1 = q;
+}
+
 // Rotation recurrence (c, s)_{k+1} = (c c1 - s s1, s c1 + c s1) on a packed pair of taps:
 // 2 FMUL2 + 2 FFMA2 per step, no register shuffling. rot1() is the bit-identical scalar form.
 struct Rot2 {
@@ -170,6 +195,13 @@ struct Rot2 {
     C1 = pk(ca, cb);
     S1 = pk(sa, sb);
     NS1 = pk(-sa, -sb);
+  }
+  __device__ __forceinline__ void init2(u64 c1, u64 s1) {
+    C = pk(1.f, 1.f);
+    S = pk(0.f, 0.f);
+    C1 = c1;
+    S1 = s1;
+    NS1 = s1 ^ 0x8000000080000000ull;
   }
   __device__ __forceinline__ void step() {
     const u64 Cn = fma2(S, NS1, mul2(C, C1));
@@ -297,14 +329,14 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
   Rot2 g2[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    float ce, se, cl, sl;
     const float Ie = Ipre[b][0], Il = Ipre[b][1];
     if (U8) {
       const float2 te = lut[(int)Ie], tl = lut[(int)Il];
-      ce = te.x; se = te.y; cl = tl.x; sl = tl.y;
+      g2[b].init(te.x, te.y, tl.x, tl.y);
     } else {
-      base_angle_f32(Ie, P, ce, se);
-      base_angle_f32(Il, P, cl, sl);
+      u64 c1, s1;
+      base_angle_f32x2(Ie, Il, P, c1, s1);
+      g2[b].init2(c1, s1);
     }
     const int re = y + P.vhi[b], rl = y + P.vlo[b] - 1;
     const bool oke = (b < P.nby) && colok && re >= 0 && re < P.H;
@@ -314,7 +346,6 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
       QS[t][b] = pk(oke ? P.qs[t][b] : 0.f, okl ? P.qs[t][b] : 0.f);
       QI[t][b] = pk(oke ? P.qsD[t][b] * Ie : 0.f, okl ? P.qsD[t][b] * Il : 0.f);
     }
-    g2[b].init(ce, se, cl, sl);
     for (int j = 0; j < P.kstep[0]; ++j) g2[b].step();
   }
   const u64 MM = pk(MAGIC, MAGIC);
@@ -1043,6 +1074,7 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
     }
   }
   P.TH = (H + best_nb - 1) / best_nb;
+  if (const char* e = std::getenv("BF_TH")) P.TH = std::max(1, std::min(H, std::atoi(e)));   // test hook
   best_nb = (H + P.TH - 1) / P.TH;
 
   longlong2* ws = nullptr;

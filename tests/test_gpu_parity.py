@@ -238,3 +238,24 @@ def test_multi_plan_case1_shared_channels(gpu):
     other, _ = make_plans(pkg, base, img.dtype, sigma_s=5.0)
     with pytest.raises(pkg.BFError):
         pkg.bilateral_filter_multi([plans[0], other], t)
+
+
+@pytest.mark.parametrize("cfg,H,W", [("cfg0", 300, 256), ("cfg2", 260, 300), ("cfg3", 200, 240),
+                                     ("cfg4", 420, 300)])
+@pytest.mark.parametrize("kernel", ["band", "ws"])
+def test_sliding_sums_are_exact(gpu, cfg, H, W, kernel, monkeypatch):
+    """The vertical state slides by adding the quantised enter taps and subtracting the leave
+    taps, which must cancel EXACTLY (the leave tap regenerates bit for bit what the enter tap, or
+    the band's initial sum, added). Every band restarts from a fresh initial sum, so the output
+    may not depend on the band height: 16-row bands and one band over the whole image must agree
+    bitwise (a one-ulp mismatch in any tap would drift and show here)."""
+    pkg, torch = gpu
+    spec = CONFIGS[cfg]
+    img = config_input(spec, H=H, W=W)
+    gp, _ = make_plans(pkg, config_params(spec), img.dtype)
+    monkeypatch.setenv("BF_KERNEL", kernel)
+    outs = []
+    for th in ("16", str(H)):
+        monkeypatch.setenv("BF_TH", th)
+        outs.append(run_gpu(pkg, torch, gp, img))
+    assert np.array_equal(outs[0], outs[1])
