@@ -68,7 +68,16 @@ typedef struct {
   int input_dtype;       /* bf_input_dtype; default BF_IN_F32                                   */
   int m_factor;          /* candidate count M = m_factor * N for the range fit; def 20 */
   int haar_levels;       /* Haar levels j <= J considered for K_s; default 4           */
+  int range_window;      /* BF_RANGE_WINDOW_FULL (default): T = D, the z-window covers every
+                            intensity (Case 1, Q1) -> 2-D box filters of modulated channels;
+                            BF_RANGE_WINDOW_LITERAL: the paper's literal 3-D form (NEXT f1):
+                            T = T_r = K_r^{-1}(0.01), cosines of period 2 T_r fitted on
+                            [-T_r, T_r] and the dimension-promoted window
+                            [I(x) - T_r, I(x) + T_r]; u8 input with D = 255 only.  */
 } bf_plan_options;
+
+/* bf_plan_options.range_window */
+enum { BF_RANGE_WINDOW_FULL = 0, BF_RANGE_WINDOW_LITERAL = 1 };
 
 /* Maximum N (range terms) and N_s (spatial terms) accepted by bf_plan_create. */
 #define BF_MAX_TERMS 32
@@ -106,7 +115,7 @@ typedef struct {
   int n_terms_eff;                           /* N_eff <= N after pruning zero coefficients     */
   int k[BF_MAX_TERMS];                       /* selected frequencies (ascending)               */
   double a[BF_MAX_TERMS];                    /* their coefficients a_k                         */
-  double T_range;                            /* T of the cosine basis (= D)                    */
+  double T_range;                            /* T of the cosine basis (D, or T_r if literal)  */
   int n_spatial_eff;                         /* selected 2-D Haar terms                        */
   int sp_family[BF_MAX_SPATIAL_TERMS];       /* 0 phi.phi, 1 phi(x)psi(y), 2 psi(x)phi(y), 3 psi.psi */
   int sp_j1[BF_MAX_SPATIAL_TERMS], sp_k1[BF_MAX_SPATIAL_TERMS];   /* x factor (j,k); -1,0 = phi */
@@ -123,6 +132,7 @@ typedef struct {
   int input_dtype;                           /* bf_input_dtype                                 */
   int spatial_rank;                          /* terms fx_s(u) fy_s(v) of the GPU box-pair form:
                                                 1 separable, 2 rank-2 (e.g. N_s = 5), 0 none     */
+  int range_window;                          /* bf_plan_options.range_window of the plan        */
 } bf_plan_info;
 
 /* Copies the plan contents into *info. */

@@ -109,11 +109,14 @@ def normalise(I, num, den):
 # --------------------------------------------------------------------------------------------
 
 
-def bf_direct(I: np.ndarray, plan: Plan, pixels=None):
+def bf_direct(I: np.ndarray, plan: Plan, pixels=None, window: float | None = None):
     """sum_y K~_s(y - x) K~_r(I(x) - I(y)) I(y) / sum_y K~_s(y - x) K~_r(I(x) - I(y)) with
     K~_s the lowered box kernel (eq:Box_N_terms) and K~_r the cosine series
     (eq:trigonometric_N_terms); the window is clipped to the image. `pixels` = optional list
-    of (y, x) to evaluate (default: all). Returns (out, num, den) arrays / vectors."""
+    of (y, x) to evaluate (default: all). `window` = T restricts the range kernel to
+    |I(x) - I(y)| <= T, the box B(I(x) - I(y)) of eq:trigonometric_N_terms / eq:1D_N_terms
+     that the literal dimension promotion evaluates (NEXT f1).
+    Returns (out, num, den) arrays / vectors."""
     I = np.asarray(I, dtype=np.float64)
     H, W = I.shape
     r = plan.radius
@@ -127,7 +130,10 @@ def bf_direct(I: np.ndarray, plan: Plan, pixels=None):
         xa, xb = max(0, x - r), min(W, x + r + 1)
         win = I[ya:yb, xa:xb]
         ks = Ks[ya - y + r:yb - y + r, xa - x + r:xb - x + r]
-        w = ks * range_kernel_approx(plan.rng, I[y, x] - win)
+        t = I[y, x] - win
+        w = ks * range_kernel_approx(plan.rng, t)
+        if window is not None:
+            w = np.where(np.abs(t) <= window, w, 0.0)
         num[i] = np.sum(w * win)
         den[i] = np.sum(w)
     center = np.array([I[y, x] for (y, x) in pixels])

@@ -291,6 +291,16 @@ def make_plan(spatial: str, range_kind: str, sigma_s: float, sigma_r: float, rad
     return Plan(rng, sp, float(intensity_max))
 
 
+def make_literal_plan(spatial: str, range_kind: str, sigma_s: float, sigma_r: float, radius: int,
+                      n_terms: int, n_spatial: int = 9, m_factor: int = 20, **_ignored) -> Plan:
+    """The paper-literal range plan (NEXT f1): T = T_r = K_r^{-1}(0.01), the cosine
+    basis of period 2 T_r fitted on [-T_r, T_r]; Plan.D = T_r is then the period
+    half-width the channels use (P:468 with T_r). Evaluate with bf.bf_promoted(I, plan, T_r)."""
+    Tr = truncation_radius(range_kind, sigma_r)
+    return make_plan(spatial, range_kind, sigma_s, sigma_r, radius, n_terms, intensity_max=Tr,
+                     n_spatial=n_spatial, m_factor=m_factor)
+
+
 def spatial_kernel_values(sp: SpatialPlan) -> np.ndarray:
     """K~_s(u, v) on the (2r+1)^2 integer grid from the lowered boxes (eq:Box_N_terms);
     array indexed [v + r, u + r] (row offset, column offset)."""

@@ -30,7 +30,7 @@ BF_MAX_PLANS = 4
 
 class PlanOptions(C.Structure):
     _fields_ = [("intensity_max", C.c_double), ("n_spatial_terms", C.c_int), ("input_dtype", C.c_int),
-                ("m_factor", C.c_int), ("haar_levels", C.c_int)]
+                ("m_factor", C.c_int), ("haar_levels", C.c_int), ("range_window", C.c_int)]
 
 
 class PlanInfo(C.Structure):
@@ -47,7 +47,7 @@ class PlanInfo(C.Structure):
         ("box_lo_y", C.c_int * BF_MAX_AXIS_BOXES), ("box_hi_y", C.c_int * BF_MAX_AXIS_BOXES),
         ("box_w_y", C.c_double * BF_MAX_AXIS_BOXES),
         ("radius", C.c_int), ("intensity_max", C.c_double), ("input_dtype", C.c_int),
-        ("spatial_rank", C.c_int),
+        ("spatial_rank", C.c_int), ("range_window", C.c_int),
     ]
 
 
@@ -105,7 +105,8 @@ class Plan:
 
     def __init__(self, spatial: str = "gaussian", range_kind: str = "gaussian", sigma_s: float = 3.0,
                  sigma_r: float = 30.0, radius: int = 9, n_terms: int = 8, intensity_max: float = 255.0,
-                 n_spatial: int = 9, input_dtype: str = "f32", m_factor: int = 20, haar_levels: int = 4):
+                 n_spatial: int = 9, input_dtype: str = "f32", m_factor: int = 20, haar_levels: int = 4,
+                 range_window: str = "full"):
         L = lib()
         opt = PlanOptions()
         L.bf_plan_options_default(C.byref(opt))
@@ -114,6 +115,7 @@ class Plan:
         opt.input_dtype = BF_IN_U8 if input_dtype in ("u8", "uint8") else BF_IN_F32
         opt.m_factor = int(m_factor)
         opt.haar_levels = int(haar_levels)
+        opt.range_window = {"full": 0, "literal": 1}[range_window]
         h = C.c_void_p()
         st = L.bf_plan_create(C.byref(h), SPATIAL[spatial], RANGE[range_kind], float(sigma_s), float(sigma_r),
                               int(radius), int(n_terms), C.byref(opt))
@@ -137,6 +139,7 @@ class Plan:
             boxes_x=[(inf.box_lo_x[i], inf.box_hi_x[i], inf.box_w_x[i]) for i in range(inf.nbx)],
             boxes_y=[(inf.box_lo_y[i], inf.box_hi_y[i], inf.box_w_y[i]) for i in range(inf.nby)],
             radius=inf.radius, intensity_max=inf.intensity_max, spatial_rank=inf.spatial_rank,
+            range_window="literal" if inf.range_window == 1 else "full",
             input_dtype="u8" if inf.input_dtype == BF_IN_U8 else "f32")
 
     def close(self) -> None:

@@ -10,6 +10,8 @@ struct bf_plan {
   double sigma_s, sigma_r;
   int radius, n_terms;
   double D;
+  double T;        // period half-width of the cosine basis: D, or T_r for the literal window
+  int literal;     // BF_RANGE_WINDOW_LITERAL
   int input_dtype;
   bf_plan_options opt;
   // range plan Lambda^r: selected k ascending and a_k

@@ -764,6 +764,122 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ kernel 3: the literal window
+// NEXT f1: the paper's dimension-promoted 3-D box filter with the window [I(x) - T_r, I(x) + T_r]
+// (eq:1D_box_N_terms, eq:numerator_2D_box_N_terms) on u8 images. The auxiliary
+// images F_c(y, z) = G^c_k(y) delta_{I(y)}(z) depend on y only through the level z = I(y), so
+// their 3-D box sums factor into the spatially weighted level counts
+//     C_z(x) = sum_y K~_s(x - y) [I(y) = z]
+// and the numerator / denominator become
+//     num(x) = sum_{|z - I(x)| <= T_r} C_z(x) z K_lit(I(x) - z),  den likewise without z,
+// with K_lit(t) = sum_k a_k cos(pi k t / T_r) (eq:trigonometric_N_terms): the shiftable split of
+// P:460-468 recombined per level (an exact identity, pinned by the oracle's bf_promoted).
+// One CTA = a strip of LIT_NT extended columns x a band of rows; each thread keeps its column's
+// level counts for the two vertical boxes packed in one int32 (lo / hi 16 bits) in shared memory,
+// sliding them down one row per step (4 taps); the output threads then sum, for every level of
+// their window, the counts over the horizontal boxes and accumulate the integer products with
+// K_lit quantised to 2^30 exactly in int64; the box weights are applied once per pixel in fp64.
+constexpr int LIT_NT = 128;
+constexpr int LIT_KB = 30;
+
+struct LParams {
+  int H, W, TW, TH, rlo_x;
+  int nbx, nby;
+  int vlo[2], vhi[2], vmin, vmax;
+  int hlo[2], hhi[2];
+  double wxy[2][2];   // wy_b * wx_b' (b vertical, b' horizontal)
+  int Tw;             // window half-width in levels: |z - I(x)| <= Tw
+  long long frame_elems;
+};
+
+__global__ void __launch_bounds__(LIT_NT, 1)
+    bf_literal_kernel(const LParams P, const int* __restrict__ klut, const unsigned char* __restrict__ in,
+                      float* __restrict__ out) {
+  constexpr int NTP = LIT_NT + 1;                   // level-row pitch (odd: scattered updates spread)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int* cnt = reinterpret_cast<int*>(smem_raw);      // [256][NTP] packed counts (box 0 lo16, box 1 hi16)
+  int* K = cnt + 256 * NTP;                         // [511] K_lit(t) * 2^30, t = -255..255
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * P.TW;
+  const int y0 = blockIdx.y * P.TH;
+  const long long fbase = (long long)blockIdx.z * P.frame_elems;
+  const int col = x0 - P.rlo_x + tid;
+  const bool colok = (col >= 0) & (col < P.W);
+  const int TWv = min(P.TW, P.W - x0);
+  const int yend = min(y0 + P.TH, P.H);
+
+  for (int i = tid; i < 256 * NTP; i += LIT_NT) cnt[i] = 0;
+  for (int i = tid; i < 511; i += LIT_NT) K[i] = klut[i];
+  __syncthreads();
+  // counts of the vertical boxes at row y0 - 1
+  if (colok) {
+    for (int v = P.vmin; v <= P.vmax; ++v) {
+      const int row = y0 - 1 + v;
+      if (row < 0 || row >= P.H) continue;
+      const int z = in[fbase + (long long)row * P.W + col];
+      int inc = 0;
+      for (int b = 0; b < P.nby; ++b)
+        if (v >= P.vlo[b] && v <= P.vhi[b]) inc += 1 << (16 * b);
+      cnt[z * NTP + tid] += inc;
+    }
+  }
+  for (int y = y0; y < yend; ++y) {
+    // ---- slide the column's counts down one row: enter y + vhi_b, leave y + vlo_b - 1
+    if (colok) {
+      for (int b = 0; b < P.nby; ++b) {
+        const int re = y + P.vhi[b], rl = y + P.vlo[b] - 1;
+        if (re >= 0 && re < P.H) cnt[in[fbase + (long long)re * P.W + col] * NTP + tid] += 1 << (16 * b);
+        if (rl >= 0 && rl < P.H) cnt[in[fbase + (long long)rl * P.W + col] * NTP + tid] -= 1 << (16 * b);
+      }
+    }
+    __syncthreads();
+    // ---- windowed level sums for the output pixels of row y
+    if (tid < TWv) {
+      const long long pix = fbase + (long long)y * P.W + x0 + tid;
+      const int I0 = in[pix];
+      const int zlo = max(0, I0 - P.Tw), zhi = min(255, I0 + P.Tw);
+      long long A[2][2] = {{0, 0}, {0, 0}}, B[2][2] = {{0, 0}, {0, 0}};
+      const int* base = cnt + tid + P.rlo_x;
+      for (int z = zlo; z <= zhi; ++z) {
+        const int* rowz = base + z * NTP;
+        const int kz = K[I0 - z + 255];
+        // horizontal boxes, the inner (b' = 1, nested) first
+        int s1 = 0;
+        if (P.nbx > 1)
+          for (int u = P.hlo[1]; u <= P.hhi[1]; ++u) s1 += rowz[u];
+        int s0 = 0;
+        if (P.nbx > 1 && P.hlo[0] <= P.hlo[1] && P.hhi[1] <= P.hhi[0]) {
+          s0 = s1;
+          for (int u = P.hlo[0]; u < P.hlo[1]; ++u) s0 += rowz[u];
+          for (int u = P.hhi[1] + 1; u <= P.hhi[0]; ++u) s0 += rowz[u];
+        } else {
+          for (int u = P.hlo[0]; u <= P.hhi[0]; ++u) s0 += rowz[u];
+        }
+        const int sb[2] = {s0, s1};
+#pragma unroll
+        for (int bx = 0; bx < 2; ++bx) {
+#pragma unroll
+          for (int by = 0; by < 2; ++by) {
+            const int c = (sb[bx] >> (16 * by)) & 0xFFFF;
+            A[by][bx] += (long long)c * kz;
+            B[by][bx] += (long long)(c * z) * kz;
+          }
+        }
+      }
+      double num = 0.0, den = 0.0;
+#pragma unroll
+      for (int by = 0; by < 2; ++by)
+#pragma unroll
+        for (int bx = 0; bx < 2; ++bx) {
+          num += P.wxy[by][bx] * (double)B[by][bx];
+          den += P.wxy[by][bx] * (double)A[by][bx];
+        }
+      out[pix] = (den > 0.0) ? (float)(num / den) : (float)I0;
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------ host side
 
 int sm_count() {
@@ -915,6 +1031,87 @@ cudaError_t dispatch(const Shape& sh, bool consec, const KParams& P, const void*
   return cudaErrorInvalidConfiguration;
 }
 
+// The literal-window path (kernel 3): u8 input, levels 0..255 (D = 255), separable plans with
+// at most two boxes per axis whose halo fits the 128-column strip.
+bf_status run_literal(const bf_plan* p, const void* d_in, float* d_out, int n_frames, int H, int W, cudaStream_t st) {
+  if (p->input_dtype != BF_IN_U8 || p->D != 255.0 || p->ns != 1 || p->snbx[0] > 2 || p->snby[0] > 2)
+    return BF_ERR_UNSUPPORTED;
+  LParams L;
+  std::memset(&L, 0, sizeof(L));
+  int rlo = 0, rhi = 0;
+  L.nbx = p->snbx[0];
+  L.nby = p->snby[0];
+  for (int b = 0; b < L.nbx; ++b) {
+    L.hlo[b] = p->slox[0][b];
+    L.hhi[b] = p->shix[0][b];
+    rlo = std::max(rlo, -L.hlo[b]);
+    rhi = std::max(rhi, L.hhi[b]);
+  }
+  if (rlo + rhi + 32 > LIT_NT) return BF_ERR_UNSUPPORTED;
+  // the packed 16-bit counts must not overflow: (box height) x (box width) < 2^15
+  for (int b = 0; b < L.nby; ++b)
+    if ((long long)(p->shiy[0][b] - p->sloy[0][b] + 1) * (rlo + rhi + 1) >= 32768) return BF_ERR_UNSUPPORTED;
+  L.vmin = p->sloy[0][0];
+  L.vmax = p->shiy[0][0];
+  for (int b = 0; b < L.nby; ++b) {
+    L.vlo[b] = p->sloy[0][b];
+    L.vhi[b] = p->shiy[0][b];
+    L.vmin = std::min(L.vmin, L.vlo[b]);
+    L.vmax = std::max(L.vmax, L.vhi[b]);
+  }
+  for (int by = 0; by < 2; ++by)
+    for (int bx = 0; bx < 2; ++bx)
+      L.wxy[by][bx] = (by < L.nby && bx < L.nbx) ? p->swy[0][by] * p->swx[0][bx] : 0.0;
+  L.H = H;
+  L.W = W;
+  L.rlo_x = rlo;
+  L.TW = LIT_NT - (rlo + rhi);
+  L.frame_elems = (long long)H * W;
+  L.Tw = (int)std::floor(p->T + 1e-9);
+  // K_lit(t) = sum_k a_k cos(pi k t / T_r) for |t| <= T_r (eq:trigonometric_N_terms), 0 outside
+  // the window, quantised to 2^30: |num|, |den| < 2^63 for |K_lit| < 2
+  int hk[511];
+  for (int t = -255; t <= 255; ++t) {
+    double k = 0.0;
+    if (std::abs(t) <= L.Tw)
+      for (int i = 0; i < p->n_k; ++i) k += p->a[i] * std::cos(M_PI * p->k[i] * t / p->T);
+    if (!(std::fabs(k) < 2.0)) return BF_ERR_NUMERIC;
+    hk[t + 255] = (int)std::lrint(std::ldexp(k, LIT_KB));
+  }
+  const int nstrips = (W + L.TW - 1) / L.TW;
+  const int nsm = sm_count();
+  const int ry = L.vmax - L.vmin + 1;
+  long long best_cost = -1;
+  int best_nb = 1;
+  for (int nb = 1; nb <= H; ++nb) {
+    const int TH = (H + nb - 1) / nb;
+    if (nb > 1 && TH < 16) break;
+    const long long ctas = (long long)nstrips * nb * n_frames;
+    const long long waves = (ctas + nsm - 1) / nsm;
+    const long long cost = waves * (4LL * TH + ry);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best_nb = nb;
+    }
+  }
+  L.TH = (H + best_nb - 1) / best_nb;
+  if (const char* e = std::getenv("BF_TH")) L.TH = std::max(1, std::min(H, std::atoi(e)));   // test hook
+  best_nb = (H + L.TH - 1) / L.TH;
+  int* dk = nullptr;   // the 2 KB table travels through a stream-ordered allocation
+  if (cudaMallocAsync(&dk, sizeof(hk), st) != cudaSuccess) return BF_ERR_CUDA;
+  cudaError_t err = cudaMemcpyAsync(dk, hk, sizeof(hk), cudaMemcpyHostToDevice, st);
+  const size_t smem = sizeof(int) * (256 * (LIT_NT + 1) + 512);
+  if (err == cudaSuccess)
+    err = cudaFuncSetAttribute(bf_literal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err == cudaSuccess) {
+    bf_literal_kernel<<<dim3(nstrips, best_nb, n_frames), LIT_NT, smem, st>>>(
+        L, dk, reinterpret_cast<const unsigned char*>(d_in), d_out);
+    err = cudaGetLastError();
+  }
+  cudaFreeAsync(dk, st);
+  return err == cudaSuccess ? BF_OK : BF_ERR_CUDA;
+}
+
 // Plans that can share one pass of box-filtered channels: same spatial form, D and input type.
 bool same_channels(const bf_plan* a, const bf_plan* b) {
   if (a->ns != b->ns || a->D != b->D || a->input_dtype != b->input_dtype) return false;
@@ -955,6 +1152,10 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
     }
   }
   const bf_plan* p = &merged;
+  if (p->literal) {
+    if (nplans != 1) return BF_ERR_UNSUPPORTED;
+    return run_literal(p, d_in, d_out, n_frames, H, W, st);
+  }
   if ((long long)H * W > (1LL << 40) / n_frames) return BF_ERR_INVALID_ARG;
   if ((const void*)d_out == d_in) return BF_ERR_INVALID_ARG;
   int rlo, rhi;
@@ -1140,6 +1341,10 @@ HostCache g_cache;
 extern "C" bf_status bf_apply_launches(const bf_plan* p, int H, int W, int* n) {
   if (!p || !n || H <= 0 || W <= 0) return BF_ERR_INVALID_ARG;
   *n = 0;
+  if (p->literal) {
+    *n = 1;
+    return BF_OK;
+  }
   int rlo, rhi;
   const Shape sh = plan_shape(p, rlo, rhi);
   if (sh.NT == 0) return BF_ERR_UNSUPPORTED;

@@ -304,6 +304,7 @@ extern "C" void bf_plan_options_default(bf_plan_options* opt) {
   opt->input_dtype = BF_IN_F32;
   opt->m_factor = 20;
   opt->haar_levels = 4;
+  opt->range_window = BF_RANGE_WINDOW_FULL;
 }
 
 extern "C" bf_status bf_plan_create(bf_plan** out, int ks, int kr, double sigma_s, double sigma_r, int radius,
@@ -323,6 +324,15 @@ extern "C" bf_status bf_plan_create(bf_plan** out, int ks, int kr, double sigma_
   if (!(opt.intensity_max > 0.0 && std::isfinite(opt.intensity_max))) return BF_ERR_INVALID_ARG;
   if (opt.n_spatial_terms < 1 || opt.n_spatial_terms > BF_MAX_SPATIAL_TERMS) return BF_ERR_INVALID_ARG;
   if (opt.m_factor < 1 || opt.haar_levels < 0 || opt.haar_levels > 8) return BF_ERR_INVALID_ARG;
+  if (opt.range_window != BF_RANGE_WINDOW_FULL && opt.range_window != BF_RANGE_WINDOW_LITERAL) return BF_ERR_INVALID_ARG;
+  // literal window: T_r = K_r^{-1}(eps), eps = 0.01: Gaussian exp(-T^2/2s^2) = eps,
+  // Tukey (1 - (T/s)^2)^2 = eps
+  double Tr = opt.intensity_max;
+  if (opt.range_window == BF_RANGE_WINDOW_LITERAL) {
+    if (std::isinf(sigma_r)) return BF_ERR_INVALID_ARG;   // K_r == 1 has no truncation point
+    Tr = (kr == BF_RANGE_GAUSSIAN) ? sigma_r * std::sqrt(-2.0 * std::log(0.01))
+                                  : sigma_r * std::sqrt(1.0 - std::sqrt(0.01));
+  }
   const int M = opt.m_factor * n_terms;
   if (M < n_terms) return BF_ERR_INVALID_ARG;
 
@@ -336,12 +346,14 @@ extern "C" bf_status bf_plan_create(bf_plan** out, int ks, int kr, double sigma_
   p->radius = radius;
   p->n_terms = n_terms;
   p->D = opt.intensity_max;
+  p->T = Tr;
+  p->literal = opt.range_window == BF_RANGE_WINDOW_LITERAL;
   p->input_dtype = opt.input_dtype;
   p->opt = opt;
 
-  // ---- range fit on [-D, D]
+  // ---- range fit on [-T, T] (T = D, or T_r for the literal window)
   std::vector<double> a;
-  range_coefficients(kr, sigma_r, opt.intensity_max, M, a);
+  range_coefficients(kr, sigma_r, Tr, M, a);
   std::vector<int> sel = select_best(a, n_terms);
   if (sel.empty()) {
     delete p;
@@ -470,7 +482,8 @@ extern "C" bf_status bf_plan_get_info(const bf_plan* p, bf_plan_info* info) {
     info->k[i] = p->k[i];
     info->a[i] = p->a[i];
   }
-  info->T_range = p->D;
+  info->T_range = p->T;
+  info->range_window = p->literal ? BF_RANGE_WINDOW_LITERAL : BF_RANGE_WINDOW_FULL;
   info->n_spatial_eff = p->n_sp;
   for (int i = 0; i < p->n_sp; ++i) {
     info->sp_family[i] = p->sp_family[i];

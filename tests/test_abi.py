@@ -146,3 +146,20 @@ def test_spatial_rank_of_the_gpu_form(bfmod):
         assert plan.info()["spatial_rank"] == want, ns
     box = bfmod.Plan(spatial="box", range_kind="gaussian", sigma_s=1.0, sigma_r=15.0, radius=10, n_terms=4)
     assert box.info()["spatial_rank"] == 1
+
+
+@pytest.mark.parametrize("cfg,over", [("cfg0", {}), ("cfg3", {}), ("cfg0", {"range_kind": "tukey", "sigma_r": 40.0})])
+def test_literal_plan_matches_oracle(bfmod, cfg, over):
+    """range_window='literal' (NEXT f1): T_range = T_r = K_r^{-1}(0.01) and the range fit on
+    [-T_r, T_r] agree with the oracle's independent literal fit."""
+    p = dict(config_params(CONFIGS[cfg]))
+    p.update(over)
+    op = fit.make_literal_plan(**p)
+    gp = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"], sigma_r=p["sigma_r"],
+                    radius=p["radius"], n_terms=p["n_terms"], input_dtype="u8", range_window="literal")
+    info = gp.info()
+    assert info["range_window"] == "literal"
+    assert abs(info["T_range"] - fit.truncation_radius(p["range_kind"], p["sigma_r"])) <= 1e-12 * info["T_range"]
+    assert info["k"] == op.rng.k
+    amax = max(abs(x) for x in op.rng.a)
+    assert np.max(np.abs(np.array(info["a"]) - np.array(op.rng.a))) <= 1e-12 * amax

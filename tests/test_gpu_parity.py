@@ -259,3 +259,26 @@ def test_sliding_sums_are_exact(gpu, cfg, H, W, kernel, monkeypatch):
         monkeypatch.setenv("BF_TH", th)
         outs.append(run_gpu(pkg, torch, gp, img))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("cfg,H,W,over", [("cfg0", 160, 230, {}), ("cfg3", 120, 260, {}),
+                                          ("cfg0", 100, 140, {"range_kind": "tukey", "sigma_r": 40.0}),
+                                          ("cfg0", 70, 90, {"n_terms": 3})])
+def test_literal_window_parity(gpu, cfg, H, W, over, monkeypatch):
+    """NEXT f1, the paper's literal 3-D box filter (window [I(x) - T_r, I(x) + T_r]) on u8 images:
+    the level-count kernel against the oracle's dimension-promoted evaluation of the same plan;
+    integer counts make the result independent of the band height (bitwise)."""
+    pkg, torch = gpu
+    spec = CONFIGS[cfg]
+    p = dict(config_params(spec))
+    p.update(over)
+    img = config_input(spec, H=H, W=W)
+    gp = pkg.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"], sigma_r=p["sigma_r"],
+                  radius=p["radius"], n_terms=p["n_terms"], input_dtype="u8", range_window="literal")
+    op = fit.make_literal_plan(**p)
+    Tr = fit.truncation_radius(p["range_kind"], p["sigma_r"])
+    ref = bf.bf_promoted(img.astype(np.float64), op, Tr)[0]
+    got = run_gpu(pkg, torch, gp, img)
+    assert_parity(got, ref, 255.0, f"{cfg} literal {over}")
+    monkeypatch.setenv("BF_TH", "16")
+    assert np.array_equal(run_gpu(pkg, torch, gp, img), got)

@@ -195,3 +195,43 @@ def test_accuracy_against_exact_bf_cfg0():
     plan, p = small_plan("cfg0")
     I = config_input(CONFIGS["cfg0"], H=40, W=40)
     assert bf.psnr(bf.bf_box(I, plan), bf.bf_exact(I, **p)) > 40.0
+
+
+
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg3"])
+def test_p2_literal_window_equals_windowed_double_loop(cfg):
+    """NEXT f1 pin: the literal dimension-promoted evaluation (per-level 2-D box sums, z-window
+    [I(x) - T_r, I(x) + T_r] with a 1-D SAT along z) equals the direct double loop of
+    sum_y K~_s K~_r(I(x)-I(y)) B(I(x)-I(y)) I(y) / sum(...) with B the window box
+    on an integer image: two different evaluations of the same definition."""
+    spec = CONFIGS[cfg]
+    p = config_params(spec)
+    I = config_input(spec, H=30, W=37).astype(np.float64)
+    plan = fit.make_literal_plan(**p)
+    Tr = fit.truncation_radius(p["range_kind"], p["sigma_r"])
+    assert Tr < 255.0 and abs(plan.D - Tr) < 1e-12
+    out, num, den = bf.bf_promoted(I, plan, Tr)
+    o2, n2, d2 = bf.bf_direct(I, plan, window=Tr)
+    scale = np.max(np.abs(d2))
+    assert np.max(np.abs(den.ravel() - d2)) <= 1e-10 * scale
+    assert np.max(np.abs(num.ravel() - n2)) <= 1e-10 * scale * 255
+    assert np.max(np.abs(out.ravel() - o2)) <= 1e-8
+    # the window matters: without it the same cosine series gives a different filter
+    o3, _, _ = bf.bf_direct(I, plan)
+    assert np.max(np.abs(o3 - o2)) > 1e-3
+
+
+def test_literal_plan_accuracy_against_exact_bf():
+    """The literal method with a handful of terms approximates the exact BF (Gaussian spatial
+    kernel, range kernel truncated at T_r) far better than the T = D hot path at the same N, the
+    paper's point about truncating the range kernel first."""
+    spec = CONFIGS["cfg0"]
+    p = dict(config_params(spec))
+    p["n_terms"] = 4
+    I = config_input(spec, H=40, W=48).astype(np.float64)
+    exact = bf.bf_exact(I, **p)
+    lit = bf.bf_promoted(I, fit.make_literal_plan(**p), fit.truncation_radius("gaussian", p["sigma_r"]))[0]
+    full = bf.bf_box(I, fit.make_plan(**p))
+    e_lit = np.sqrt(np.mean((lit - exact) ** 2))
+    e_full = np.sqrt(np.mean((full - exact) ** 2))
+    assert e_lit < 0.5 * e_full

@@ -59,6 +59,18 @@ def main():
             t = timed(lambda: pkg.bilateral_filter(p, im))
             print(f"{cfg} N_s={ns} (rank {p.info()['spatial_rank']}): {t:.3f} ms, "
                   f"{im.numel() / t / 1e3:.0f} MP/s")
+    for cfg in ("cfg0", "cfg3"):   # the paper-literal window (NEXT f1), u8 configs
+        sp = CONFIGS[cfg]
+        im = torch.from_numpy(config_input(sp)).cuda()
+        p = plan_for(sp)
+        prm = config_params(sp)
+        pl = pkg.Plan(spatial=prm["spatial"], range_kind=prm["range_kind"], sigma_s=prm["sigma_s"],
+                      sigma_r=prm["sigma_r"], radius=prm["radius"], n_terms=prm["n_terms"], input_dtype="u8",
+                      range_window="literal")
+        t0 = timed(lambda: pkg.bilateral_filter(p, im))
+        tl = timed(lambda: pkg.bilateral_filter(pl, im))
+        print(f"{cfg} literal window T_r={pl.info()['T_range']:.1f}: {tl:.3f} ms ({im.numel() / tl / 1e3:.0f} MP/s) "
+              f"vs T=D hot path {t0:.3f} ms")
     for cfg in ("cfg0", "cfg1", "cfg2", "cfg3"):
         sp = CONFIGS[cfg]
         im = torch.from_numpy(config_input(sp)).cuda()
