@@ -72,6 +72,7 @@ struct KParams {
   double invD, D;
   int pass;                   // 0 = only pass; 1 = first; 2 = middle; 3 = last
   int ngrp, nseg, seglen;     // walkers: 32-channel groups x row segments
+  int wpar;                   // paired-load walker: parity of box 1's leave stream (0 / 1), -1 = scalar walker
   int f_off, l_off;           // shared-memory carve-up: U' [4 nk][NT+1] int, F [TW][4 MAXK + 4] int,
                               // LUTs (u8) float2[256] + double2[256]
 };
@@ -487,6 +488,125 @@ __device__ __forceinline__ void walk_row(const KParams& P, const int* Ur, int sr
   }
 }
 
+// walk_row for symmetric odd-width boxes (one box per stream pair, at most two pairs), with
+// 64-bit shared-memory loads: the U' rows have an even pitch and the segments start at even x, so
+// every leave stream has a fixed parity (box 0 even, box 1 even iff LPAR1 == 0) and its enter
+// stream the opposite one (the box width 2r + 1 is odd). Even streams read aligned pairs; odd
+// streams carry the high word of the previous pair. Half the load instructions of walk_row for
+// the same shared-memory words. Same arithmetic as walk_row (bitwise equal results).
+template <int M, int FPX, int LPAR1>
+__device__ __forceinline__ void walk_row_pairs(const KParams& P, const int* Ur, int srow, int* Fcol, int xs, int xe) {
+  int lo[M], hi[M], ax[M], Hs[M];
+  const int* base[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int t = (M == 2 && P.ns == 2) ? m : 0;    // rank 2: one box per term
+    const int b = (M == 2 && P.ns == 2) ? 0 : m;
+    lo[m] = P.hlo[t][b];
+    hi[m] = P.hhi[t][b];
+    ax[m] = P.ax[t][b];
+    base[m] = Ur + t * srow;
+  }
+  // initial window sums at xs (inner box first, the outer one reuses it when nested)
+#pragma unroll
+  for (int m = M - 1; m >= 0; --m) {
+    const int* U = base[m];
+    int a = xs + lo[m], b = xs + hi[m];
+    int acc = 0, a2 = b + 1, b2 = b;
+    if (M == 2 && m == 0 && P.ns == 1 && lo[0] <= lo[1] && hi[1] <= hi[0]) {
+      acc = Hs[1];
+      a2 = xs + hi[1] + 1;
+      b = xs + lo[1] - 1;
+    }
+    int s0 = 0, s1 = 0;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      int j = pass ? a2 : a;
+      const int je = pass ? b2 : b;
+      if (j <= je && ((reinterpret_cast<uintptr_t>(U + j) >> 2) & 1)) s0 += U[j++];   // to an even word
+      for (; j + 1 <= je; j += 2) {
+        const int2 v = *reinterpret_cast<const int2*>(U + j);
+        s0 += v.x;
+        s1 += v.y;
+      }
+      if (j <= je) s0 += U[j];
+    }
+    Hs[m] = acc + s0 + s1;
+  }
+  const long long frnd = P.frnd;
+  const int fsh = P.fsh;
+  // stream pointers: leave at xs + lo (parity lpar), enter at xs + hi + 1 (parity 1 - lpar)
+  const int* pl[M];
+  const int* pe[M];
+  int cl[M], ce[M];   // carried high words of the odd streams
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int lpar = (m == 1) ? LPAR1 : 0;
+    pl[m] = base[m] + xs + lo[m] - lpar;          // even word
+    pe[m] = base[m] + xs + hi[m] + 1 - (1 - lpar);
+    if (lpar) cl[m] = pl[m][1];
+    else ce[m] = pe[m][1];
+  }
+  int* pf = Fcol + xs * FPX;
+  int x = xs;
+  for (; x + 4 <= xe; x += 4) {
+    int e[M][4], l[M][4];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int lpar = (m == 1) ? LPAR1 : 0;
+      if (lpar == 0) {   // leave even: aligned pairs at pl, pl + 2; enter odd: carry + pairs at pe + 2, pe + 4
+        const int2 a0 = *reinterpret_cast<const int2*>(pl[m]);
+        const int2 a1 = *reinterpret_cast<const int2*>(pl[m] + 2);
+        const int2 b0 = *reinterpret_cast<const int2*>(pe[m] + 2);
+        const int2 b1 = *reinterpret_cast<const int2*>(pe[m] + 4);
+        l[m][0] = a0.x; l[m][1] = a0.y; l[m][2] = a1.x; l[m][3] = a1.y;
+        e[m][0] = ce[m]; e[m][1] = b0.x; e[m][2] = b0.y; e[m][3] = b1.x;
+        ce[m] = b1.y;
+      } else {           // leave odd, enter even
+        const int2 a0 = *reinterpret_cast<const int2*>(pl[m] + 2);
+        const int2 a1 = *reinterpret_cast<const int2*>(pl[m] + 4);
+        const int2 b0 = *reinterpret_cast<const int2*>(pe[m]);
+        const int2 b1 = *reinterpret_cast<const int2*>(pe[m] + 2);
+        l[m][0] = cl[m]; l[m][1] = a0.x; l[m][2] = a0.y; l[m][3] = a1.x;
+        cl[m] = a1.y;
+        e[m][0] = b0.x; e[m][1] = b0.y; e[m][2] = b1.x; e[m][3] = b1.y;
+      }
+      pl[m] += 4;
+      pe[m] += 4;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      long long f = frnd;
+#pragma unroll
+      for (int m = 0; m < M; ++m) f += (long long)ax[m] * Hs[m];
+      pf[j * FPX] = (int)(f >> fsh);
+#pragma unroll
+      for (int m = 0; m < M; ++m) Hs[m] += e[m][j] - l[m][j];
+    }
+    pf += 4 * FPX;
+  }
+  for (; x < xe; ++x) {   // tail (< 4 outputs): scalar
+    long long f = frnd;
+#pragma unroll
+    for (int m = 0; m < M; ++m) f += (long long)ax[m] * Hs[m];
+    *pf = (int)(f >> fsh);
+    pf += FPX;
+#pragma unroll
+    for (int m = 0; m < M; ++m) Hs[m] += base[m][x + 1 + hi[m]] - base[m][x + lo[m]];
+  }
+}
+
+// H(y) dispatch: the paired-load walker when the host found the box layout for it (wpar >= 0)
+template <int NBX, int NS, int FPX>
+__device__ __forceinline__ void walk(const KParams& P, const int* Ur, int srow, int* Fcol, int xs, int xe) {
+  constexpr int M = NS * NBX;
+  if constexpr (M <= 2) {
+    if (P.wpar == 0) return walk_row_pairs<M, FPX, 0>(P, Ur, srow, Fcol, xs, xe);
+    if (P.wpar == 1) return walk_row_pairs<M, FPX, 1>(P, Ur, srow, Fcol, xs, xe);
+  }
+  walk_row<NBX, NS, FPX>(P, Ur, srow, Fcol, xs, xe);
+}
+
 // C: num = sum_k W_c F_Ic + W_s F_Is, den = sum_k W_c F_c + W_s F_s for one output pixel with
 // the weights a_k cos / sin(k pi I(x) / D) in fp64 rounded to int32 (exact int64 sums); then
 // out = D num / den (den <= 0: out = I(x), Q18), or the int64 pair to the multi-pass workspace.
@@ -672,7 +792,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     bf_ws_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out, longlong2* __restrict__ ws) {
   constexpr int NS = Form<FORM>::NS, NB = Form<FORM>::NBY, NBX = Form<FORM>::NBX;
   constexpr int NT = WS_V;
-  constexpr int UP = NT + 1;
+  constexpr int UP = NT + 2;           // even pitch (== 2 mod 64): the paired-load walker's LDS.64 are conflict-free
   constexpr int FPX = 4 * MAXK + 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int srow = 4 * P.nk * UP;                                             // ints per term's U' rows
@@ -734,7 +854,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       bar_sync(BAR_U_FULL + b, NUF);
       if (y - y0 >= 2) bar_sync(BAR_F_EMPTY + b, NFF);
       if (wact && xs < xe)
-        walk_row<NBX, NS, FPX>(P, Ubuf + b * ustride + wslot * UP + P.rlo_x, srow, Fbuf + b * fstride + wslot, xs, xe);
+        walk<NBX, NS, FPX>(P, Ubuf + b * ustride + wslot * UP + P.rlo_x, srow, Fbuf + b * fstride + wslot, xs, xe);
       bar_arrive(BAR_U_EMPTY + b, NUF);
       bar_arrive(BAR_F_FULL + b, NFF);
     }
@@ -905,7 +1025,7 @@ size_t smem_layout(KParams& P, int NT, int MAXK, bool u8) {
 // warp-specialised kernel: two U' row buffers and two F row buffers
 size_t smem_layout_ws(KParams& P, int MAXK, bool u8) {
   auto up16 = [](size_t v) { return (v + 15) / 16 * 16; };
-  size_t off = up16(sizeof(int) * 2 * P.ns * 4 * (size_t)P.nk * (WS_V + 1));
+  size_t off = up16(sizeof(int) * 2 * P.ns * 4 * (size_t)P.nk * (WS_V + 2));
   P.f_off = (int)off;
   off = up16(off + sizeof(int) * 2 * (size_t)P.TW * (4 * MAXK + 4));
   P.l_off = (int)off;
@@ -1314,6 +1434,25 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
     if (const char* e = std::getenv("BF_NSEG")) nseg = std::max(1, std::min(max_tasks / P.ngrp, std::atoi(e)));  // tuning hook
     P.nseg = nseg;
     P.seglen = (TW + nseg - 1) / nseg;
+    P.seglen += P.seglen & 1;   // even segment starts (paired loads)
+    // paired-load walker: every horizontal box symmetric [-r_b, r_b] (odd width), at most two
+    // boxes in all; box 0 the widest (its leave stream at rlo - r_0 = 0 is even)
+    P.wpar = -1;
+    {
+      int m = 0, r0 = -1, r1 = -1;
+      bool ok = true;
+      for (int t = 0; t < ns; ++t)
+        for (int b = 0; b < p->snbx[t]; ++b) {
+          if (p->slox[t][b] != -p->shix[t][b]) ok = false;
+          if (m == 0) r0 = p->shix[t][b];
+          else r1 = p->shix[t][b];
+          ++m;
+        }
+      // (warp-specialised kernel only: the barrier-interval kernel measured faster with its
+      // scalar walker and the odd pitch)
+      if (sh.wsk && ok && m <= 2 && r0 == rlo && (m == 1 || r1 <= r0)) P.wpar = (m == 2) ? ((r0 - r1) & 1) : 0;
+      if (const char* e = std::getenv("BF_SCALAR_WALK")) P.wpar = std::atoi(e) ? -1 : P.wpar;   // tuning hook
+    }
     P.pass = (passes == 1) ? 0 : (pass == 0 ? 1 : (pass == passes - 1 ? 3 : 2));
     err = u8 ? dispatch<true>(sh, consec, P, d_in, d_out, ws, grid, st)
              : dispatch<false>(sh, consec, P, d_in, d_out, ws, grid, st);
