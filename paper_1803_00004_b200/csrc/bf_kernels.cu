@@ -596,6 +596,82 @@ __device__ __forceinline__ void walk_row_pairs(const KParams& P, const int* Ur, 
   }
 }
 
+// F from exclusive prefix rows (no window init, no dependency between outputs): Q[e] holds
+// sum_{e' < e} U'[e'] (mod 2^32: the box differences are exact because every box sum fits
+// int32), so H_m(x) = Q[x + hi + 1] - Q[x + lo] is read with the same paired loads as the
+// walker's enter / leave streams.
+template <int M, int FPX, int LPAR1>
+__device__ __forceinline__ void prefix_row_pairs(const KParams& P, const int* Ur, int srow, int* Fcol, int xs, int xe) {
+  int lo[M], hi[M], ax[M];
+  const int* base[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int t = (M == 2 && P.ns == 2) ? m : 0;    // rank 2: one box per term
+    const int b = (M == 2 && P.ns == 2) ? 0 : m;
+    lo[m] = P.hlo[t][b];
+    hi[m] = P.hhi[t][b];
+    ax[m] = P.ax[t][b];
+    base[m] = Ur + t * srow;
+  }
+  const long long frnd = P.frnd;
+  const int fsh = P.fsh;
+  // stream pointers: leave at xs + lo (parity lpar), enter at xs + hi + 1 (parity 1 - lpar)
+  const int* pl[M];
+  const int* pe[M];
+  int cl[M], ce[M];   // carried high words of the odd streams
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int lpar = (m == 1) ? LPAR1 : 0;
+    pl[m] = base[m] + xs + lo[m] - lpar;          // even word
+    pe[m] = base[m] + xs + hi[m] + 1 - (1 - lpar);
+    if (lpar) cl[m] = pl[m][1];
+    else ce[m] = pe[m][1];
+  }
+  int* pf = Fcol + xs * FPX;
+  int x = xs;
+  for (; x + 4 <= xe; x += 4) {
+    int e[M][4], l[M][4];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int lpar = (m == 1) ? LPAR1 : 0;
+      if (lpar == 0) {   // leave even: aligned pairs at pl, pl + 2; enter odd: carry + pairs at pe + 2, pe + 4
+        const int2 a0 = *reinterpret_cast<const int2*>(pl[m]);
+        const int2 a1 = *reinterpret_cast<const int2*>(pl[m] + 2);
+        const int2 b0 = *reinterpret_cast<const int2*>(pe[m] + 2);
+        const int2 b1 = *reinterpret_cast<const int2*>(pe[m] + 4);
+        l[m][0] = a0.x; l[m][1] = a0.y; l[m][2] = a1.x; l[m][3] = a1.y;
+        e[m][0] = ce[m]; e[m][1] = b0.x; e[m][2] = b0.y; e[m][3] = b1.x;
+        ce[m] = b1.y;
+      } else {           // leave odd, enter even
+        const int2 a0 = *reinterpret_cast<const int2*>(pl[m] + 2);
+        const int2 a1 = *reinterpret_cast<const int2*>(pl[m] + 4);
+        const int2 b0 = *reinterpret_cast<const int2*>(pe[m]);
+        const int2 b1 = *reinterpret_cast<const int2*>(pe[m] + 2);
+        l[m][0] = cl[m]; l[m][1] = a0.x; l[m][2] = a0.y; l[m][3] = a1.x;
+        cl[m] = a1.y;
+        e[m][0] = b0.x; e[m][1] = b0.y; e[m][2] = b1.x; e[m][3] = b1.y;
+      }
+      pl[m] += 4;
+      pe[m] += 4;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      long long f = frnd;
+#pragma unroll
+      for (int m = 0; m < M; ++m) f += (long long)ax[m] * (e[m][j] - l[m][j]);   // box sum = Q[hi+1] - Q[lo]
+      pf[j * FPX] = (int)(f >> fsh);
+    }
+    pf += 4 * FPX;
+  }
+  for (; x < xe; ++x) {   // tail (< 4 outputs): scalar
+    long long f = frnd;
+#pragma unroll
+    for (int m = 0; m < M; ++m) f += (long long)ax[m] * (base[m][x + 1 + hi[m]] - base[m][x + lo[m]]);
+    *pf = (int)(f >> fsh);
+    pf += FPX;
+  }
+}
+
 // H(y) dispatch: the paired-load walker when the host found the box layout for it (wpar >= 0)
 template <int NBX, int NS, int FPX>
 __device__ __forceinline__ void walk(const KParams& P, const int* Ur, int srow, int* Fcol, int xs, int xe) {
@@ -780,7 +856,9 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
 //   warps 16-19 C: combine / normalise / store, F -> output
 // Registers are redistributed with setmaxnreg (V 152, H 56, C 56; 640 x 96 at launch).
 constexpr int WS_V = 256, WS_H = 256, WS_C = 128, WS_THREADS = WS_V + WS_H + WS_C;
+constexpr int WS_S = 64, WS_F = WS_H - WS_S;   // H role: 2 prefix-scan warps + 6 box-difference warps
 constexpr int BAR_U_FULL = 1, BAR_U_EMPTY = 3, BAR_F_FULL = 5, BAR_F_EMPTY = 7;   // + buffer index
+constexpr int BAR_Q_FULL = 9;                                                     // + buffer index
 
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
@@ -809,8 +887,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   const long long fbase = (long long)blockIdx.z * P.frame_elems;
   const int TWv = min(P.TW, P.W - x0);
   const int yend = min(y0 + P.TH, P.H);
-  constexpr int NUF = WS_V + WS_H;   // participants of the U' barriers
-  constexpr int NFF = WS_H + WS_C;   // participants of the F barriers
+  constexpr int NUF = WS_V + WS_H;   // participants of the U' barriers (walker form)
+  constexpr int NFF = WS_H + WS_C;   // participants of the F barriers (walker form)
+  const bool pre = P.wpar >= 0;      // prefix form of the H role (scan + difference warps)
+  const int nUfull = pre ? WS_V + WS_S : NUF, nUempty = pre ? WS_V + WS_F : NUF, nF = pre ? WS_F + WS_C : NFF;
 
   fill_luts<U8>(P, lut, lut64, tid, WS_THREADS);
   __syncthreads();
@@ -833,14 +913,79 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         Icur[bb][1] = Ipre[bb][1];
       }
       if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col, colok, y + 1, Ipre);
-      if (y - y0 >= 2) bar_sync(BAR_U_EMPTY + b, NUF);
+      if (y - y0 >= 2) bar_sync(BAR_U_EMPTY + b, nUempty);
       v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + b * ustride + tid);
-      bar_arrive(BAR_U_FULL + b, NUF);
+      bar_arrive(BAR_U_FULL + b, nUfull);
     }
-    // drain: the walkers' last releases
-    for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_U_EMPTY + ((y - y0) & 1), NUF);
+    // drain: the H role's last releases
+    for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_U_EMPTY + ((y - y0) & 1), nUempty);
+  } else if (tid < WS_V + WS_H && P.wpar >= 0) {
+    // ------------------------------------------------------------ H role, prefix form
+    // 2 scan warps turn each U' row into its exclusive prefix in place (lane = channel slot,
+    // one pass over the 256 columns with paired loads); 6 difference warps then read every box
+    // sum as Q[x + hi + 1] - Q[x + lo] (no window init, no chain between outputs)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    constexpr int M = NS * NBX;
+    const int ht = tid - WS_V;
+    if (ht < WS_S) {
+      const int slot = ht;
+      const bool act = slot < 4 * P.nk;
+      for (int y = y0; y < yend; ++y) {
+        const int b = (y - y0) & 1;
+        bar_sync(BAR_U_FULL + b, WS_V + WS_S);
+        if (act) {
+#pragma unroll
+          for (int t = 0; t < NS; ++t) {
+            int* Q = Ubuf + b * ustride + t * srow + slot * UP;
+            // 8 columns per step: their local exclusive prefix is a short tree of adds off the
+            // carry chain, so the chain is one add per 8 columns (the scan is latency bound)
+            int carry = 0;
+#pragma unroll 2
+            for (int e = 0; e < NT; e += 8) {
+              // (rows are 8-byte aligned: pitch NT + 2)
+              const int2 a0 = *reinterpret_cast<const int2*>(Q + e), a1 = *reinterpret_cast<const int2*>(Q + e + 2);
+              const int2 b0 = *reinterpret_cast<const int2*>(Q + e + 4), b1 = *reinterpret_cast<const int2*>(Q + e + 6);
+              const int p1 = a0.x, p2 = a0.x + a0.y, p3 = p2 + a1.x, p4 = p3 + a1.y;
+              const int q1 = b0.x, q2 = b0.x + b0.y, q3 = q2 + b1.x, q4 = q3 + b1.y;
+              const int c4 = carry + p4;
+              *reinterpret_cast<int2*>(Q + e) = make_int2(carry, carry + p1);
+              *reinterpret_cast<int2*>(Q + e + 2) = make_int2(carry + p2, carry + p3);
+              *reinterpret_cast<int2*>(Q + e + 4) = make_int2(c4, c4 + q1);
+              *reinterpret_cast<int2*>(Q + e + 6) = make_int2(c4 + q2, c4 + q3);
+              carry = c4 + q4;
+            }
+            Q[NT] = carry;
+          }
+        }
+        bar_arrive(BAR_Q_FULL + b, WS_S + WS_F);
+      }
+    } else {
+      const int ft = ht - WS_S;
+      const int wgrp = (ft >> 5) % P.ngrp;
+      const int wseg = (ft >> 5) / P.ngrp;
+      const int wslot = wgrp * 32 + (ft & 31);
+      const bool wact = (wslot < 4 * P.nk) && (wseg < P.nseg);
+      const int xs = wseg * P.seglen;
+      const int xe = min(xs + P.seglen, TWv);
+      for (int y = y0; y < yend; ++y) {
+        const int b = (y - y0) & 1;
+        bar_sync(BAR_Q_FULL + b, WS_S + WS_F);
+        if (y - y0 >= 2) bar_sync(BAR_F_EMPTY + b, WS_F + WS_C);
+        if constexpr (M <= 2) {
+          if (wact && xs < xe) {
+            const int* Qr = Ubuf + b * ustride + wslot * UP + P.rlo_x;
+            int* Fr = Fbuf + b * fstride + wslot;
+            if (P.wpar == 0) prefix_row_pairs<M, FPX, 0>(P, Qr, srow, Fr, xs, xe);
+            else prefix_row_pairs<M, FPX, 1>(P, Qr, srow, Fr, xs, xe);
+          }
+        }
+        bar_arrive(BAR_U_EMPTY + b, WS_V + WS_F);
+        bar_arrive(BAR_F_FULL + b, WS_F + WS_C);
+      }
+      for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_F_EMPTY + ((y - y0) & 1), WS_F + WS_C);
+    }
   } else if (tid < WS_V + WS_H) {
-    // ------------------------------------------------------------ H role
+    // ------------------------------------------------------------ H role, walkers (general boxes)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     const int ht = tid - WS_V;
     const int wgrp = (ht >> 5) % P.ngrp;
@@ -871,7 +1016,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         const int o = ct + j * WS_C;
         Iv[j] = (o < TWv) ? load_pixel(in, U8, fbase + (long long)y * P.W + x0 + o) : 0.f;
       }
-      bar_sync(BAR_F_FULL + b, NFF);
+      bar_sync(BAR_F_FULL + b, nF);
 #pragma unroll 1
       for (int j = 0; j < 2; ++j) {
         const int o = ct + j * WS_C;
@@ -879,7 +1024,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
           combine_pixel<MAXK, U8, CONSEC, FULL, MULTI>(P, lut64, reinterpret_cast<const int4*>(Fbuf + b * fstride + o * FPX),
                                                 Iv[j], fbase + (long long)y * P.W + x0 + o, out, ws);
       }
-      bar_arrive(BAR_F_EMPTY + b, NFF);
+      bar_arrive(BAR_F_EMPTY + b, nF);
     }
   }
 }
@@ -1116,12 +1261,11 @@ Shape plan_shape(const bf_plan* p, int& rlo, int& rhi) {
   }
   const int halo = rlo + rhi;
   const int nk = p->n_k;
-  // warp-specialised for NT = 256 except at 13-16 terms, where the barrier-interval kernel with
-  // two resident CTAs measured 2% faster on cfg2
+  // warp-specialised for NT = 256 (its prefix-form H role measured 2.32 vs 2.50 ms on cfg2)
   if (halo <= 128) {
     sh.NT = 256;
     sh.MAXK = (nk <= 8 || p->ns == 2) ? 8 : 16;
-    sh.wsk = sh.form != 4 && (nk <= 12 || p->ns == 2);
+    sh.wsk = sh.form != 4;
   } else {
     sh.NT = 512;
     sh.MAXK = 8;
@@ -1427,7 +1571,7 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
       }
     }
     // walker segments: ngrp * nseg warps; long segments amortise the initial window sums
-    const int max_tasks = sh.wsk ? WS_H / 32 : sh.NT / 32;
+    const int max_tasks = sh.wsk ? WS_H / 32 : sh.NT / 32;   // (prefix form: WS_F / 32, set below)
     int nseg = std::max(1, max_tasks / P.ngrp);
     const int min_len = sh.wsk ? 24 : std::max(32, 2 * (rlo + rhi + 1) / 3);
     while (nseg > 1 && (TW + nseg - 1) / nseg < min_len) --nseg;
@@ -1452,6 +1596,11 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
       // scalar walker and the odd pitch)
       if (sh.wsk && ok && m <= 2 && r0 == rlo && (m == 1 || r1 <= r0)) P.wpar = (m == 2) ? ((r0 - r1) & 1) : 0;
       if (const char* e = std::getenv("BF_SCALAR_WALK")) P.wpar = std::atoi(e) ? -1 : P.wpar;   // tuning hook
+    }
+    if (sh.wsk && P.wpar >= 0) {   // prefix form: the box differences need no long segments
+      P.nseg = std::max(1, (WS_F / 32) / P.ngrp);
+      P.seglen = (TW + P.nseg - 1) / P.nseg;
+      P.seglen += P.seglen & 1;
     }
     P.pass = (passes == 1) ? 0 : (pass == 0 ? 1 : (pass == passes - 1 ? 3 : 2));
     err = u8 ? dispatch<true>(sh, consec, P, d_in, d_out, ws, grid, st)
