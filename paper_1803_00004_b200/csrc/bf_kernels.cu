@@ -322,9 +322,11 @@ __device__ __forceinline__ void load_taps(const KParams& P, const void* __restri
 
 // V(y): slide the vertical state one row (enter / leave taps of every box, packed in pairs)
 // and store U' = U >> ush of every channel slot at Ucol[slot * UP].
-template <int MAXK, int NB, int NS, bool U8, bool CONSEC, bool FULL, int UP>
+struct GroupSync;   // per-channel-group barriers of the warp-specialised kernel (defined with it)
+
+template <int MAXK, int NB, int NS, bool U8, bool CONSEC, bool FULL, int UP, class Hook = GroupSync>
 __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool colok, int y, const float (&Ipre)[NB][2],
-                                      int (&U)[NS * 4 * MAXK], int* Ucol) {
+                                      int (&U)[NS * 4 * MAXK], int* Ucol, const Hook* hook = nullptr) {
   const int nk = P.nk;
   u64 QS[NS][NB], QI[NS][NB];
   Rot2 g2[NB];
@@ -353,6 +355,7 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
 #pragma unroll
   for (int i = 0; i < MAXK; ++i) {
     if (FULL || i < nk) {
+      if (hook && (i & 7) == 0) hook->begin(i >> 3);   // channel group i / 8 starts: its buffer free
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         if (i > 0) {
@@ -375,6 +378,7 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           Ucol[(t * 4 * nk + 4 * i + c) * UP] = U[t * 4 * MAXK + 4 * i + c] >> P.ush;
+      if (hook && ((i & 7) == 7 || i + 1 == nk)) hook->end(i >> 3);   // channel group i / 8 written
     }
   }
 }
@@ -849,28 +853,46 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
 }
 
 // ------------------------------------------------------------------ kernel 2: warp-specialised
-// Three warp roles connected by double-buffered shared-memory rows and named barriers, so the
-// vertical pass of row y+1 overlaps the horizontal pass of row y and the combine of row y-1:
-//   warps 0-7   V: one thread per extended column (NT = 256), producer of U'(y) rows
-//   warps 8-15  H: walkers, lane = channel slot, warp = (slot group, segment); U' -> F rows
-//   warps 16-19 C: combine / normalise / store, F -> output
-// Registers are redistributed with setmaxnreg (V 152, H 56, C 56; 640 x 96 at launch).
-constexpr int WS_V = 256, WS_H = 256, WS_C = 128, WS_THREADS = WS_V + WS_H + WS_C;
-constexpr int WS_S = 64, WS_F = WS_H - WS_S;   // H role: 2 prefix-scan warps + 6 box-difference warps
-constexpr int BAR_U_FULL = 1, BAR_U_EMPTY = 3, BAR_F_FULL = 5, BAR_F_EMPTY = 7;   // + buffer index
-constexpr int BAR_Q_FULL = 9;                                                     // + buffer index
+// Four warp roles connected by double-buffered shared-memory rows and named barriers, pipelined
+// per 32-channel group (a group = 8 terms = one walker warp's lanes), so the vertical pass of
+// row y+1, the horizontal pass of row y and the combine of row y-1 overlap:
+//   warps 0-7    V: one thread per extended column (NT = 256), writes U'(y) group by group
+//   warps 8-9    S: warp g turns group g's U' rows into exclusive prefix rows Q in place
+//   warps 10-15  F: box sums Q[x + hi + 1] - Q[x + lo] -> F rows (warp = group x segment)
+//   warps 16-19  C: combine / normalise / store, F -> output
+// Registers are redistributed with setmaxnreg (V 152, S / F / C 56; 640 x 96 at launch). Named
+// barriers (all 16, barrier 0 reused after the opening __syncthreads):
+//   U_FULL(b,g) 0-3   V arrive, S_g sync        U_EMPTY(b,g) 4-7  F_g arrive, V sync
+//   Q_FULL(b,g) 8-11  S_g arrive, F_g sync      F_FULL(b) 12-13   F arrive, C sync
+//   F_EMPTY(b) 14-15  C arrive, F sync          (b = row parity, g = channel group)
+constexpr int WS_V = 256, WS_S = 64, WS_F = 192, WS_C = 128, WS_THREADS = WS_V + WS_S + WS_F + WS_C;
+constexpr int WS_H = WS_S + WS_F;
+constexpr int BAR_U_FULL = 0, BAR_U_EMPTY = 4, BAR_Q_FULL = 8, BAR_F_FULL = 12, BAR_F_EMPTY = 14;
 
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// V's per-group hooks: wait until group g's buffer of this row parity is free (F_g done with
+// row y-2), and publish group g once written
+struct GroupSync {
+  int b, nfree, nfull;
+  bool wait;
+  __device__ __forceinline__ void begin(int g) const {
+    if (wait) bar_sync(BAR_U_EMPTY + 2 * b + g, nfree);
+  }
+  __device__ __forceinline__ void end(int g) const { bar_arrive(BAR_U_FULL + 2 * b + g, nfull); }
+};
+
 template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL, bool MULTI>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     bf_ws_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out, longlong2* __restrict__ ws) {
   constexpr int NS = Form<FORM>::NS, NB = Form<FORM>::NBY, NBX = Form<FORM>::NBX;
+  constexpr int M = NS * NBX;
+  static_assert(M <= 2, "the prefix-form H role handles at most two horizontal boxes");
   constexpr int NT = WS_V;
-  constexpr int UP = NT + 2;           // even pitch (== 2 mod 64): the paired-load walker's LDS.64 are conflict-free
+  constexpr int UP = NT + 2;           // even pitch (== 2 mod 64): conflict-free LDS.64 with lanes = channels
   constexpr int FPX = 4 * MAXK + 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int srow = 4 * P.nk * UP;                                             // ints per term's U' rows
@@ -887,10 +909,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   const long long fbase = (long long)blockIdx.z * P.frame_elems;
   const int TWv = min(P.TW, P.W - x0);
   const int yend = min(y0 + P.TH, P.H);
-  constexpr int NUF = WS_V + WS_H;   // participants of the U' barriers (walker form)
-  constexpr int NFF = WS_H + WS_C;   // participants of the F barriers (walker form)
-  const bool pre = P.wpar >= 0;      // prefix form of the H role (scan + difference warps)
-  const int nUfull = pre ? WS_V + WS_S : NUF, nUempty = pre ? WS_V + WS_F : NUF, nF = pre ? WS_F + WS_C : NFF;
+  const int ngrp = P.ngrp;                       // channel groups (1 or 2)
+  const int nfw = (WS_F / 32) / ngrp;            // F warps per group
+  const int n_uempty = WS_V + 32 * nfw;          // U_EMPTY: F_g arrive, V sync
+  const int n_ufull = WS_V + 32;                 // U_FULL: V arrive, S_g sync
+  const int n_qfull = 32 + 32 * nfw;             // Q_FULL: S_g arrive, F_g sync
+  constexpr int n_f = WS_F + WS_C;               // F_FULL / F_EMPTY
 
   fill_luts<U8>(P, lut, lut64, tid, WS_THREADS);
   __syncthreads();
@@ -913,36 +937,32 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         Icur[bb][1] = Ipre[bb][1];
       }
       if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col, colok, y + 1, Ipre);
-      if (y - y0 >= 2) bar_sync(BAR_U_EMPTY + b, nUempty);
-      v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + b * ustride + tid);
-      bar_arrive(BAR_U_FULL + b, nUfull);
+      const GroupSync hook{b, n_uempty, n_ufull, y - y0 >= 2};
+      v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + b * ustride + tid, &hook);
     }
-    // drain: the H role's last releases
-    for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_U_EMPTY + ((y - y0) & 1), nUempty);
-  } else if (tid < WS_V + WS_H && P.wpar >= 0) {
-    // ------------------------------------------------------------ H role, prefix form
-    // 2 scan warps turn each U' row into its exclusive prefix in place (lane = channel slot,
-    // one pass over the 256 columns with paired loads); 6 difference warps then read every box
-    // sum as Q[x + hi + 1] - Q[x + lo] (no window init, no chain between outputs)
+    // drain: the F warps' last releases
+    for (int y = max(y0, yend - 2); y < yend; ++y)
+      for (int g = 0; g < ngrp; ++g) bar_sync(BAR_U_EMPTY + 2 * ((y - y0) & 1) + g, n_uempty);
+  } else if (tid < WS_V + WS_S) {
+    // ------------------------------------------------------------ S role: prefix scans
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-    constexpr int M = NS * NBX;
-    const int ht = tid - WS_V;
-    if (ht < WS_S) {
-      const int slot = ht;
+    const int g = (tid - WS_V) >> 5;
+    if (g < ngrp) {
+      const int slot = 32 * g + (tid & 31);
       const bool act = slot < 4 * P.nk;
       for (int y = y0; y < yend; ++y) {
         const int b = (y - y0) & 1;
-        bar_sync(BAR_U_FULL + b, WS_V + WS_S);
+        bar_sync(BAR_U_FULL + 2 * b + g, n_ufull);
         if (act) {
 #pragma unroll
           for (int t = 0; t < NS; ++t) {
             int* Q = Ubuf + b * ustride + t * srow + slot * UP;
-            // 8 columns per step: their local exclusive prefix is a short tree of adds off the
-            // carry chain, so the chain is one add per 8 columns (the scan is latency bound)
+            // exclusive prefix in place, 8 columns per step: the carry chain is one add per 8
+            // columns (rows are 8-byte aligned: pitch NT + 2); int32 wrap-around keeps every box
+            // difference exact (each box sum fits int32)
             int carry = 0;
 #pragma unroll 2
             for (int e = 0; e < NT; e += 8) {
-              // (rows are 8-byte aligned: pitch NT + 2)
               const int2 a0 = *reinterpret_cast<const int2*>(Q + e), a1 = *reinterpret_cast<const int2*>(Q + e + 2);
               const int2 b0 = *reinterpret_cast<const int2*>(Q + e + 4), b1 = *reinterpret_cast<const int2*>(Q + e + 6);
               const int p1 = a0.x, p2 = a0.x + a0.y, p3 = p2 + a1.x, p4 = p3 + a1.y;
@@ -957,53 +977,33 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             Q[NT] = carry;
           }
         }
-        bar_arrive(BAR_Q_FULL + b, WS_S + WS_F);
+        bar_arrive(BAR_Q_FULL + 2 * b + g, n_qfull);
       }
-    } else {
-      const int ft = ht - WS_S;
-      const int wgrp = (ft >> 5) % P.ngrp;
-      const int wseg = (ft >> 5) / P.ngrp;
-      const int wslot = wgrp * 32 + (ft & 31);
-      const bool wact = (wslot < 4 * P.nk) && (wseg < P.nseg);
-      const int xs = wseg * P.seglen;
-      const int xe = min(xs + P.seglen, TWv);
-      for (int y = y0; y < yend; ++y) {
-        const int b = (y - y0) & 1;
-        bar_sync(BAR_Q_FULL + b, WS_S + WS_F);
-        if (y - y0 >= 2) bar_sync(BAR_F_EMPTY + b, WS_F + WS_C);
-        if constexpr (M <= 2) {
-          if (wact && xs < xe) {
-            const int* Qr = Ubuf + b * ustride + wslot * UP + P.rlo_x;
-            int* Fr = Fbuf + b * fstride + wslot;
-            if (P.wpar == 0) prefix_row_pairs<M, FPX, 0>(P, Qr, srow, Fr, xs, xe);
-            else prefix_row_pairs<M, FPX, 1>(P, Qr, srow, Fr, xs, xe);
-          }
-        }
-        bar_arrive(BAR_U_EMPTY + b, WS_V + WS_F);
-        bar_arrive(BAR_F_FULL + b, WS_F + WS_C);
-      }
-      for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_F_EMPTY + ((y - y0) & 1), WS_F + WS_C);
     }
   } else if (tid < WS_V + WS_H) {
-    // ------------------------------------------------------------ H role, walkers (general boxes)
+    // ------------------------------------------------------------ F role: box differences
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-    const int ht = tid - WS_V;
-    const int wgrp = (ht >> 5) % P.ngrp;
-    const int wseg = (ht >> 5) / P.ngrp;
-    const int wslot = wgrp * 32 + (ht & 31);
-    const bool wact = (wslot < 4 * P.nk) && (wseg < P.nseg);
-    const int xs = wseg * P.seglen;
+    const int ft = tid - WS_V - WS_S;
+    const int g = (ft >> 5) % ngrp;
+    const int seg = (ft >> 5) / ngrp;
+    const int slot = 32 * g + (ft & 31);
+    const bool act = (slot < 4 * P.nk) && (seg < P.nseg);
+    const int xs = seg * P.seglen;
     const int xe = min(xs + P.seglen, TWv);
     for (int y = y0; y < yend; ++y) {
       const int b = (y - y0) & 1;
-      bar_sync(BAR_U_FULL + b, NUF);
-      if (y - y0 >= 2) bar_sync(BAR_F_EMPTY + b, NFF);
-      if (wact && xs < xe)
-        walk<NBX, NS, FPX>(P, Ubuf + b * ustride + wslot * UP + P.rlo_x, srow, Fbuf + b * fstride + wslot, xs, xe);
-      bar_arrive(BAR_U_EMPTY + b, NUF);
-      bar_arrive(BAR_F_FULL + b, NFF);
+      bar_sync(BAR_Q_FULL + 2 * b + g, n_qfull);
+      if (y - y0 >= 2) bar_sync(BAR_F_EMPTY + b, n_f);
+      if (act && xs < xe) {
+        const int* Qr = Ubuf + b * ustride + slot * UP + P.rlo_x;
+        int* Fr = Fbuf + b * fstride + slot;
+        if (P.wpar == 0) prefix_row_pairs<M, FPX, 0>(P, Qr, srow, Fr, xs, xe);
+        else prefix_row_pairs<M, FPX, 1>(P, Qr, srow, Fr, xs, xe);
+      }
+      bar_arrive(BAR_U_EMPTY + 2 * b + g, n_uempty);
+      bar_arrive(BAR_F_FULL + b, n_f);
     }
-    for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_F_EMPTY + ((y - y0) & 1), NFF);
+    for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_F_EMPTY + ((y - y0) & 1), n_f);
   } else {
     // ------------------------------------------------------------ C role
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
@@ -1016,15 +1016,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         const int o = ct + j * WS_C;
         Iv[j] = (o < TWv) ? load_pixel(in, U8, fbase + (long long)y * P.W + x0 + o) : 0.f;
       }
-      bar_sync(BAR_F_FULL + b, nF);
+      bar_sync(BAR_F_FULL + b, n_f);
 #pragma unroll 1
       for (int j = 0; j < 2; ++j) {
         const int o = ct + j * WS_C;
         if (o < TWv)
           combine_pixel<MAXK, U8, CONSEC, FULL, MULTI>(P, lut64, reinterpret_cast<const int4*>(Fbuf + b * fstride + o * FPX),
-                                                Iv[j], fbase + (long long)y * P.W + x0 + o, out, ws);
+                                                       Iv[j], fbase + (long long)y * P.W + x0 + o, out, ws);
       }
-      bar_arrive(BAR_F_EMPTY + b, nF);
+      bar_arrive(BAR_F_EMPTY + b, n_f);
     }
   }
 }
@@ -1512,6 +1512,23 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
 
   const int passes = (p->n_k + sh.MAXK - 1) / sh.MAXK;
   if (nplans > 1 && passes > 1) return BF_ERR_UNSUPPORTED;   // shared channels must fit one pass
+  // paired-load layout of the horizontal boxes (warp-specialised kernel): every box symmetric
+  // [-r_b, r_b] (odd width), at most two boxes in all, box 0 the widest (leave stream even)
+  int wpar = -1;
+  {
+    int m = 0, r0 = -1, r1 = -1;
+    bool ok = true;
+    for (int t = 0; t < ns; ++t)
+      for (int b = 0; b < p->snbx[t]; ++b) {
+        if (p->slox[t][b] != -p->shix[t][b]) ok = false;
+        if (m == 0) r0 = p->shix[t][b];
+        else r1 = p->shix[t][b];
+        ++m;
+      }
+    if (ok && m <= 2 && r0 == rlo && (m == 1 || r1 <= r0)) wpar = (m == 2) ? ((r0 - r1) & 1) : 0;
+  }
+  if (wpar < 0) sh.wsk = false;
+  if ((4 * std::min(sh.MAXK, p->n_k) + 31) / 32 > 2) sh.wsk = false;   // two scan warps
   P.nplans = nplans;
   P.plan_stride = (long long)H * W;
   if (sh.wsk) {   // the double-buffered rows must fit the 227 KB of shared memory
@@ -1579,25 +1596,8 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
     P.nseg = nseg;
     P.seglen = (TW + nseg - 1) / nseg;
     P.seglen += P.seglen & 1;   // even segment starts (paired loads)
-    // paired-load walker: every horizontal box symmetric [-r_b, r_b] (odd width), at most two
-    // boxes in all; box 0 the widest (its leave stream at rlo - r_0 = 0 is even)
-    P.wpar = -1;
-    {
-      int m = 0, r0 = -1, r1 = -1;
-      bool ok = true;
-      for (int t = 0; t < ns; ++t)
-        for (int b = 0; b < p->snbx[t]; ++b) {
-          if (p->slox[t][b] != -p->shix[t][b]) ok = false;
-          if (m == 0) r0 = p->shix[t][b];
-          else r1 = p->shix[t][b];
-          ++m;
-        }
-      // (warp-specialised kernel only: the barrier-interval kernel measured faster with its
-      // scalar walker and the odd pitch)
-      if (sh.wsk && ok && m <= 2 && r0 == rlo && (m == 1 || r1 <= r0)) P.wpar = (m == 2) ? ((r0 - r1) & 1) : 0;
-      if (const char* e = std::getenv("BF_SCALAR_WALK")) P.wpar = std::atoi(e) ? -1 : P.wpar;   // tuning hook
-    }
-    if (sh.wsk && P.wpar >= 0) {   // prefix form: the box differences need no long segments
+    P.wpar = sh.wsk ? wpar : -1;
+    if (sh.wsk) {   // F warps of the warp-specialised kernel: (WS_F / 32) / ngrp segments per group
       P.nseg = std::max(1, (WS_F / 32) / P.ngrp);
       P.seglen = (TW + P.nseg - 1) / P.nseg;
       P.seglen += P.seglen & 1;
