@@ -216,6 +216,7 @@ def run_ours(args, spec):
     sptr = stream.cuda_stream
     H, W = img.shape
     launches = bfp.launches(plan, H, W)     # kernel launches per bf_apply (bf_apply_launches)
+    lcfg = bfp.config(plan, H, W)            # the kernel and launch shape bf_apply enqueues (bf_apply_config)
 
     def step():
         bfp.apply(plan, img.data_ptr(), out.data_ptr(), H, W, sptr)
@@ -283,7 +284,9 @@ def run_ours(args, spec):
         "config": config_dict(spec, True, world),
         "roofline": {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "T lane-op/s",
                      "frac": alu_achieved / alu_peak, "traffic": traffic_per_launch(spec.name),
-                     "kernel": "bf_band_kernel", "launches_per_step": launches,
+                     "kernel": lcfg["kernel"], "launches_per_step": launches,
+                     "launch": {"threads_per_cta": lcfg["threads_per_cta"], "grid": list(lcfg["grid"]),
+                                "tile": list(lcfg["tile"]), "smem_bytes": lcfg["smem_bytes"]},
                      "algorithmic_ops_per_step": alu_ops,
                      "peak_source": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (B200_PROFILING.md unit counts)",
                      "note": "SURVEY 8(d): >= 8 FP32-lane ops per channel-pixel, C = 4 N_eff channels"},

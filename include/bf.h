@@ -186,6 +186,23 @@ BF_API bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float* h_o
  */
 BF_API bf_status bf_apply_launches(const bf_plan* plan, int H, int W, int* n_launches);
 
+/* Launch configuration bf_apply_batched(plan, ., ., n_frames, H, W, .) enqueues (bf_apply is
+ * n_frames = 1): kernel name (a static string owned by the library), threads per CTA, grid
+ * (strips x bands x frames), output tile (columns per strip, rows per band), dynamic shared
+ * memory per CTA and the number of launches (passes). Pure host computation, no device work;
+ * the kernel choice and band height follow the same rules (and BF_KERNEL / BF_TH tuning
+ * variables) as the apply call. Errors as bf_apply_launches. */
+typedef struct bf_launch_config {
+  int n_launches;
+  const char* kernel;
+  int threads_per_cta;
+  int grid_x, grid_y, grid_z;
+  int tile_w, tile_h;
+  size_t smem_bytes;
+} bf_launch_config;
+
+BF_API bf_status bf_apply_config(const bf_plan* plan, int n_frames, int H, int W, bf_launch_config* cfg);
+
 /* Static string for a status code. */
 BF_API const char* bf_status_string(bf_status s);
 

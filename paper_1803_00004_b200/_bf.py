@@ -23,14 +23,20 @@ RANGE = {"gaussian": BF_RANGE_GAUSSIAN, "tukey": BF_RANGE_TUKEY}
 
 #: every symbol include/bf.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bf_plan_options_default", "bf_plan_create", "bf_plan_destroy", "bf_plan_get_info", "bf_apply",
-           "bf_apply_batched", "bf_apply_host", "bf_apply_launches", "bf_apply_multi", "bf_status_string",
-           "bf_version")
+           "bf_apply_batched", "bf_apply_config", "bf_apply_host", "bf_apply_launches", "bf_apply_multi",
+           "bf_status_string", "bf_version")
 BF_MAX_PLANS = 4
 
 
 class PlanOptions(C.Structure):
     _fields_ = [("intensity_max", C.c_double), ("n_spatial_terms", C.c_int), ("input_dtype", C.c_int),
                 ("m_factor", C.c_int), ("haar_levels", C.c_int), ("range_window", C.c_int)]
+
+
+class LaunchConfig(C.Structure):
+    _fields_ = [("n_launches", C.c_int), ("kernel", C.c_char_p), ("threads_per_cta", C.c_int), ("grid_x", C.c_int),
+                ("grid_y", C.c_int), ("grid_z", C.c_int), ("tile_w", C.c_int), ("tile_h", C.c_int),
+                ("smem_bytes", C.c_size_t)]
 
 
 class PlanInfo(C.Structure):
@@ -87,6 +93,8 @@ def lib() -> C.CDLL:
         L.bf_apply_multi.restype = C.c_int
         L.bf_apply_launches.argtypes = [P, C.c_int, C.c_int, C.POINTER(C.c_int)]
         L.bf_apply_launches.restype = C.c_int
+        L.bf_apply_config.argtypes = [P, C.c_int, C.c_int, C.c_int, C.POINTER(LaunchConfig)]
+        L.bf_apply_config.restype = C.c_int
         L.bf_status_string.argtypes = [C.c_int]
         L.bf_status_string.restype = C.c_char_p
         L.bf_version.argtypes = []
@@ -184,6 +192,15 @@ def launches(plan: Plan, H: int, W: int) -> int:
     n = C.c_int(0)
     _check(lib().bf_apply_launches(plan.handle, int(H), int(W), C.byref(n)), "bf_apply_launches")
     return n.value
+
+
+def config(plan: Plan, H: int, W: int, n_frames: int = 1) -> dict:
+    """Launch configuration of bf_apply(_batched) for this shape (bf_apply_config): kernel name,
+    threads per CTA, grid, output tile, dynamic shared memory, launches."""
+    c = LaunchConfig()
+    _check(lib().bf_apply_config(plan.handle, int(n_frames), int(H), int(W), C.byref(c)), "bf_apply_config")
+    return {"kernel": c.kernel.decode(), "launches": c.n_launches, "threads_per_cta": c.threads_per_cta,
+            "grid": (c.grid_x, c.grid_y, c.grid_z), "tile": (c.tile_w, c.tile_h), "smem_bytes": c.smem_bytes}
 
 
 def version() -> str:

@@ -43,7 +43,7 @@ constexpr float MAGIC = 12582912.0f;              // 1.5 * 2^23
 constexpr int MAGIC_BITS = 0x4B400000;            // bit pattern of MAGIC
 constexpr double MAGIC64 = 6755399441055744.0;    // 1.5 * 2^52: low word of fma(x, s, MAGIC64) = rint(x*s)
 constexpr int QBITS_MAX = 22;                     // channel quantisation (the FFMA trick's range)
-constexpr int ABITS = 27;                         // horizontal integer box weights
+constexpr int ABITS = 30;                         // horizontal integer box weights (mulhi multipliers)
 constexpr int MAXB = 4;                           // boxes per axis
 constexpr int MAXP = BF_MAX_PLANS;                // range plans of one bf_apply_multi
 
@@ -60,9 +60,8 @@ struct KParams {
   int urnd, ush;              // U' = (U + urnd) >> ush; urnd is folded into the initial state
   int nbx[2];                 // horizontal boxes of term s
   int hlo[2][MAXB], hhi[2][MAXB];   // their column offsets (inclusive)
-  int ax[2][MAXB];            // their integer weights round(wx_sb / max|wx| * 2^27)
-  int fsh;                    // F = (sum_b ax_b H_b + frnd) >> fsh fits int32
-  long long frnd;
+  int ax[2][MAXB];            // their integer weights round(wx_sb / max|wx| * 2^abits):
+                              // F = sum_tb mulhi(H_tb, ax_tb) (high words of the int64 products)
   int nk;                     // terms of this pass
   int kstep[BF_MAX_TERMS];    // Chebyshev steps before term i (term 0: from k = 0)
   double aw[BF_MAX_PLANS][16];   // a_k * 2^wbits of each range plan (bf_apply_multi; one plan otherwise)
@@ -73,6 +72,7 @@ struct KParams {
   int pass;                   // 0 = only pass; 1 = first; 2 = middle; 3 = last
   int ngrp, nseg, seglen;     // walkers: 32-channel groups x row segments
   int wpar;                   // paired-load walker: parity of box 1's leave stream (0 / 1), -1 = scalar walker
+  int wv;                     // kernel 2b: extended columns written and scanned (TW + halo rounded up to 8)
   int f_off, l_off;           // shared-memory carve-up: U' [4 nk][NT+1] int, F [TW][4 MAXK + 4] int,
                               // LUTs (u8) float2[256] + double2[256]
 };
@@ -95,6 +95,13 @@ __device__ __forceinline__ int diff_bits(u64 v) {
   int a, b;
   asm("mov.b64 {%0, %1}, %2;" : "=r"(a), "=r"(b) : "l"(v));
   return a - b;
+}
+// c + (int64) a * b as ONE IMAD.WIDE (the compiler otherwise widens a shifted-and-narrowed operand
+// to a full 64 x 64 product)
+__device__ __forceinline__ long long mad_wide(int a, int b, long long c) {
+  long long r;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+  return r;
 }
 __device__ __forceinline__ int quant(float x, float s) { return __float_as_int(fmaf(x, s, MAGIC)) - MAGIC_BITS; }
 
@@ -384,7 +391,7 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
 }
 
 // H(y) for one channel slot over output columns [xs, xe): slide the exact int32 horizontal box
-// sums H_tb of U'_t (term t, box b) and write F = (sum_tb ax_tb H_tb + frnd) >> fsh (exact int64,
+// sums H_tb of U'_t (term t, box b) and write F = sum_tb mulhi(H_tb, ax_tb) (int64 products,
 // narrowed) to Fcol[x * FPX]. Ur[o + u] is U'_0 at output column o, offset u; U'_t = Ur + t*srow.
 template <int NB, int NS, int FPX>
 __device__ __forceinline__ void walk_row(const KParams& P, const int* Ur, int srow, int* Fcol, int xs, int xe) {
@@ -432,8 +439,6 @@ __device__ __forceinline__ void walk_row(const KParams& P, const int* Ur, int sr
       }
       Hs[m] = acc + (a0 + a1) + (a2 + a3);
     }
-  const long long frnd = P.frnd;
-  const int fsh = P.fsh;
   const int* pe[M];
   const int* pl[M];
 #pragma unroll
@@ -472,20 +477,20 @@ __device__ __forceinline__ void walk_row(const KParams& P, const int* Ur, int sr
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      long long f = frnd;
+      int f = 0;
 #pragma unroll
-      for (int m = 0; m < M; ++m) f += (long long)ax[m] * Hs[m];
-      pf[j * FPX] = (int)(f >> fsh);
+      for (int m = 0; m < M; ++m) f += __mulhi(Hs[m], ax[m]);
+      pf[j * FPX] = f;
 #pragma unroll
       for (int m = 0; m < M; ++m) Hs[m] += e[m][j] - l[m][j];
     }
     pf += 4 * FPX;
   }
   for (int j = 0; x < xe; ++x, ++j) {   // tail (< 4 outputs)
-    long long f = frnd;
+    int f = 0;
 #pragma unroll
-    for (int m = 0; m < M; ++m) f += (long long)ax[m] * Hs[m];
-    *pf = (int)(f >> fsh);
+    for (int m = 0; m < M; ++m) f += __mulhi(Hs[m], ax[m]);
+    *pf = f;
     pf += FPX;
 #pragma unroll
     for (int m = 0; m < M; ++m) Hs[m] += pe[m][j] - pl[m][j];
@@ -537,8 +542,6 @@ __device__ __forceinline__ void walk_row_pairs(const KParams& P, const int* Ur, 
     }
     Hs[m] = acc + s0 + s1;
   }
-  const long long frnd = P.frnd;
-  const int fsh = P.fsh;
   // stream pointers: leave at xs + lo (parity lpar), enter at xs + hi + 1 (parity 1 - lpar)
   const int* pl[M];
   const int* pe[M];
@@ -580,20 +583,20 @@ __device__ __forceinline__ void walk_row_pairs(const KParams& P, const int* Ur, 
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      long long f = frnd;
+      int f = 0;
 #pragma unroll
-      for (int m = 0; m < M; ++m) f += (long long)ax[m] * Hs[m];
-      pf[j * FPX] = (int)(f >> fsh);
+      for (int m = 0; m < M; ++m) f += __mulhi(Hs[m], ax[m]);
+      pf[j * FPX] = f;
 #pragma unroll
       for (int m = 0; m < M; ++m) Hs[m] += e[m][j] - l[m][j];
     }
     pf += 4 * FPX;
   }
   for (; x < xe; ++x) {   // tail (< 4 outputs): scalar
-    long long f = frnd;
+    int f = 0;
 #pragma unroll
-    for (int m = 0; m < M; ++m) f += (long long)ax[m] * Hs[m];
-    *pf = (int)(f >> fsh);
+    for (int m = 0; m < M; ++m) f += __mulhi(Hs[m], ax[m]);
+    *pf = f;
     pf += FPX;
 #pragma unroll
     for (int m = 0; m < M; ++m) Hs[m] += base[m][x + 1 + hi[m]] - base[m][x + lo[m]];
@@ -617,8 +620,6 @@ __device__ __forceinline__ void prefix_row_pairs(const KParams& P, const int* Ur
     ax[m] = P.ax[t][b];
     base[m] = Ur + t * srow;
   }
-  const long long frnd = P.frnd;
-  const int fsh = P.fsh;
   // stream pointers: leave at xs + lo (parity lpar), enter at xs + hi + 1 (parity 1 - lpar)
   const int* pl[M];
   const int* pe[M];
@@ -660,18 +661,18 @@ __device__ __forceinline__ void prefix_row_pairs(const KParams& P, const int* Ur
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      long long f = frnd;
+      int f = 0;
 #pragma unroll
-      for (int m = 0; m < M; ++m) f += (long long)ax[m] * (e[m][j] - l[m][j]);   // box sum = Q[hi+1] - Q[lo]
-      pf[j * FPX] = (int)(f >> fsh);
+      for (int m = 0; m < M; ++m) f += __mulhi(e[m][j] - l[m][j], ax[m]);   // box sum = Q[hi+1] - Q[lo]
+      pf[j * FPX] = f;
     }
     pf += 4 * FPX;
   }
   for (; x < xe; ++x) {   // tail (< 4 outputs): scalar
-    long long f = frnd;
+    int f = 0;
 #pragma unroll
-    for (int m = 0; m < M; ++m) f += (long long)ax[m] * (base[m][x + 1 + hi[m]] - base[m][x + lo[m]]);
-    *pf = (int)(f >> fsh);
+    for (int m = 0; m < M; ++m) f += __mulhi(base[m][x + 1 + hi[m]] - base[m][x + lo[m]], ax[m]);
+    *pf = f;
     pf += FPX;
   }
 }
@@ -867,6 +868,7 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
 //   F_EMPTY(b) 14-15  C arrive, F sync          (b = row parity, g = channel group)
 constexpr int WS_V = 256, WS_S = 64, WS_F = 192, WS_C = 128, WS_THREADS = WS_V + WS_S + WS_F + WS_C;
 constexpr int WS_H = WS_S + WS_F;
+constexpr int KERN_BAND = 0, KERN_WS = 1, KERN_WS2 = 2;
 constexpr int BAR_U_FULL = 0, BAR_U_EMPTY = 4, BAR_Q_FULL = 8, BAR_F_FULL = 12, BAR_F_EMPTY = 14;
 
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -1029,6 +1031,207 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ kernel 2b: fused box-difference + combine
+// Three roles; the F row buffer of kernel 2 is gone, which pays for 384 extended columns
+// (TW = min(320, 384 - halo) outputs: halo overhead 1.33x instead of 1.6x at r = 48):
+//   warps 0-11   V: one thread per extended column, writes U'(y) group by group (as kernel 2)
+//   warps 12-13  S: warp g turns group g's U' rows into exclusive prefix rows Q in place
+//   warps 14-23  FH: one thread per output pixel: for every channel slot of group g,
+//                F = sum_b mulhi(Q[x + hi_b + 1] - Q[x + lo_b], ax_b) (lanes = consecutive
+//                x: conflict-free), accumulated straight into the exact int64 num / den with the
+//                pixel's fp64 combine weights; then out = D num / den
+// setmaxnreg: V 112, S / FH 48 (768 x 80 at launch). Named barriers:
+//   U_FULL(b,g) 0-3   V arrive, S_g sync        U_EMPTY(b,g) 4-7  FH arrive, V sync
+//   Q_FULL(b,g) 8-11  S_g arrive, FH sync       (b = row parity, g = channel group)
+constexpr int W2_V = 384, W2_S = 64, W2_H = 320, W2_THREADS = W2_V + W2_S + W2_H;
+constexpr int W2_UP = W2_V + 4;   // == 4 mod 32: conflict-free LDS.128 / STS.128 with lanes = channels
+
+// Exclusive prefix of one U' row in place, 8 columns per step (two 16-byte loads / stores, one
+// IADD3 per column); int32 wrap-around keeps every box difference exact. Q[n] = total.
+__device__ __forceinline__ void prefix_row(int* Q, int n) {
+  int carry = 0;
+#pragma unroll 2
+  for (int e = 0; e < n; e += 8) {
+    const int4 a = *reinterpret_cast<const int4*>(Q + e), b = *reinterpret_cast<const int4*>(Q + e + 4);
+    const int o1 = carry + a.x;
+    const int o2 = carry + a.x + a.y;
+    const int o3 = o1 + a.y + a.z;
+    const int o4 = o2 + a.z + a.w;
+    const int o5 = o3 + a.w + b.x;
+    const int o6 = o4 + b.x + b.y;
+    const int o7 = o5 + b.y + b.z;
+    const int o8 = o6 + b.z + b.w;
+    *reinterpret_cast<int4*>(Q + e) = make_int4(carry, o1, o2, o3);
+    *reinterpret_cast<int4*>(Q + e + 4) = make_int4(o4, o5, o6, o7);
+    carry = o8;
+  }
+  Q[n] = carry;
+}
+
+// out = D num / den (den <= 0: I(x), Q18), or the int64 pair to / from the multi-pass workspace
+__device__ __forceinline__ void finish_pixel(const KParams& P, long long num, long long den, float Ic, long long pix,
+                                             float* __restrict__ out, longlong2* __restrict__ ws) {
+  if (P.pass == 1) {
+    ws[pix] = make_longlong2(num, den);
+    return;
+  }
+  if (P.pass >= 2) {
+    const longlong2 acc = ws[pix];
+    num += acc.x;
+    den += acc.y;
+  }
+  if (P.pass == 2) ws[pix] = make_longlong2(num, den);
+  else out[pix] = (den > 0) ? (float)(P.D * (double)num / (double)den) : Ic;
+}
+
+template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL>
+__global__ void __launch_bounds__(W2_THREADS, 1)
+    bf_ws2_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out, longlong2* __restrict__ ws) {
+  constexpr int NS = Form<FORM>::NS, NB = Form<FORM>::NBY, NBX = Form<FORM>::NBX;
+  constexpr int M = NS * NBX;
+  static_assert(NS == 1 && M <= 2, "the FH role handles separable forms with at most two x boxes");
+  constexpr int UP = W2_UP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int srow = 4 * P.nk * UP;                                             // ints per term's U' rows
+  const int ustride = NS * srow;                                              // ints per U' buffer
+  int* Ubuf = reinterpret_cast<int*>(smem_raw);                               // [2][NS][4 nk][UP]
+  float2* lut = reinterpret_cast<float2*>(smem_raw + P.l_off);
+  double2* lut64 = reinterpret_cast<double2*>(lut + 256);
+
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * P.TW;
+  const int y0 = blockIdx.y * P.TH;
+  const long long fbase = (long long)blockIdx.z * P.frame_elems;
+  const int TWv = min(P.TW, P.W - x0);
+  const int yend = min(y0 + P.TH, P.H);
+  const int wv = P.wv;                            // extended columns scanned (multiple of 8, <= W2_V)
+  const int ngrp = P.ngrp;                        // channel groups (1 or 2)
+  constexpr int n_ufull = W2_V + 32;              // U_FULL: V arrive, S_g sync
+  constexpr int n_uempty = W2_V + W2_H;           // U_EMPTY: FH arrive, V sync
+  constexpr int n_qfull = 32 + W2_H;              // Q_FULL: S_g arrive, FH sync
+
+  fill_luts<U8>(P, lut, lut64, tid, W2_THREADS);
+  __syncthreads();
+
+  if (tid < W2_V) {
+    // ------------------------------------------------------------ V role
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
+    const int col = x0 - P.rlo_x + tid;
+    const bool colok = (col >= 0) & (col < P.W) & (tid < wv);
+    const bool vwork = (tid & ~31) < wv;          // warps wholly past the scanned columns only sync
+    int U[NS * 4 * MAXK];
+    if (vwork) v_init<MAXK, NB, NS, U8, CONSEC, FULL>(P, in, lut, fbase, col, colok, y0, U);
+    float Ipre[NB][2];
+    if (vwork) load_taps<NB, U8>(P, in, fbase, col, colok, y0, Ipre);
+    for (int y = y0; y < yend; ++y) {
+      const int b = (y - y0) & 1;
+      const GroupSync hook{b, n_uempty, n_ufull, y - y0 >= 2};
+      if (vwork) {
+        float Icur[NB][2];
+#pragma unroll
+        for (int bb = 0; bb < NB; ++bb) {
+          Icur[bb][0] = Ipre[bb][0];
+          Icur[bb][1] = Ipre[bb][1];
+        }
+        if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col, colok, y + 1, Ipre);
+        v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + b * ustride + tid, &hook);
+      } else {
+        for (int g = 0; g < ngrp; ++g) {
+          hook.begin(g);
+          hook.end(g);
+        }
+      }
+    }
+    // drain: the FH warps' last releases
+    for (int y = max(y0, yend - 2); y < yend; ++y)
+      for (int g = 0; g < ngrp; ++g) bar_sync(BAR_U_EMPTY + 2 * ((y - y0) & 1) + g, n_uempty);
+  } else if (tid < W2_V + W2_S) {
+    // ------------------------------------------------------------ S role: prefix scans
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
+    const int g = (tid - W2_V) >> 5;
+    if (g < ngrp) {
+      const int slot = 32 * g + (tid & 31);
+      const bool act = slot < 4 * P.nk;
+      for (int y = y0; y < yend; ++y) {
+        const int b = (y - y0) & 1;
+        bar_sync(BAR_U_FULL + 2 * b + g, n_ufull);
+        if (act) {
+#pragma unroll
+          for (int t = 0; t < NS; ++t) prefix_row(Ubuf + b * ustride + t * srow + slot * UP, wv);
+        }
+        bar_arrive(BAR_Q_FULL + 2 * b + g, n_qfull);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ FH role
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
+    const int o = tid - W2_V - W2_S;
+    const bool act = o < TWv;
+    if ((o & ~31) >= TWv) {   // warp wholly past the strip: only the barriers
+      for (int y = y0; y < yend; ++y) {
+        const int b = (y - y0) & 1;
+        for (int g = 0; g < ngrp; ++g) {
+          bar_sync(BAR_Q_FULL + 2 * b + g, n_qfull);
+          bar_arrive(BAR_U_EMPTY + 2 * b + g, n_uempty);
+        }
+      }
+      return;
+    }
+    const int oc = act ? o : 0;
+    // Q offsets (extended index o + rlo) of the x boxes: F = sum_b mulhi(Q[e_b] - Q[l_b], ax_b)
+    const bool two = (M == 2) && P.nbx[0] == 2;
+    const int e0 = oc + P.rlo_x + P.hhi[0][0] + 1, l0 = oc + P.rlo_x + P.hlo[0][0];
+    const int e1 = two ? oc + P.rlo_x + P.hhi[0][1] + 1 : e0, l1 = two ? oc + P.rlo_x + P.hlo[0][1] : l0;
+    const int ax0 = P.ax[0][0], ax1 = two ? P.ax[0][1] : 0;
+    const long long prow = fbase + x0 + oc;
+    float Inext = act ? load_pixel(in, U8, prow + (long long)y0 * P.W) : 0.f;
+    for (int y = y0; y < yend; ++y) {
+      const int b = (y - y0) & 1;
+      const float Ic = Inext;
+      if (act && y + 1 < yend) Inext = load_pixel(in, U8, prow + (long long)(y + 1) * P.W);
+      double c1, s1;
+      if (U8) {
+        const double2 t = lut64[(int)Ic];
+        c1 = t.x;
+        s1 = t.y;
+      } else {
+        base_angle_f64(Ic, P.invD, c1, s1);
+      }
+      Cheb64 gk;
+      gk.init(c1, s1);
+      for (int j = 0; j < P.kstep[0]; ++j) gk.step();
+      const int* Qb = Ubuf + b * ustride;
+      long long num = 0, den = 0;
+#pragma unroll
+      for (int i = 0; i < MAXK; ++i) {
+        if (FULL || i < P.nk) {
+          if ((i & 7) == 0) bar_sync(BAR_Q_FULL + 2 * b + (i >> 3), n_qfull);
+          if (i > 0) {
+            if (CONSEC) gk.step();
+            else
+              for (int j = 0; j < P.kstep[i]; ++j) gk.step();
+          }
+          const int wc = __double2loint(fma(gk.c, P.aw[0][i], MAGIC64));
+          const int wsn = __double2loint(fma(gk.s, P.aw[0][i], MAGIC64));
+          int F[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int* q = Qb + (4 * i + c) * UP;
+            F[c] = __mulhi(q[e0] - q[l0], ax0);
+            if (M == 2) F[c] += __mulhi(q[e1] - q[l1], ax1);
+          }
+          den = mad_wide(wc, F[0], den);
+          den = mad_wide(wsn, F[1], den);
+          num = mad_wide(wc, F[2], num);
+          num = mad_wide(wsn, F[3], num);
+          if ((i & 7) == 7 || i + 1 == P.nk) bar_arrive(BAR_U_EMPTY + 2 * b + (i >> 3), n_uempty);
+        }
+      }
+      if (act) finish_pixel(P, num, den, Ic, prow + (long long)y * P.W, out, ws);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ kernel 3: the literal window
 // NEXT f1: the paper's dimension-promoted 3-D box filter with the window [I(x) - T_r, I(x) + T_r]
 // (eq:1D_box_N_terms, eq:numerator_2D_box_N_terms) on u8 images. The auxiliary
@@ -1168,6 +1371,14 @@ size_t smem_layout(KParams& P, int NT, int MAXK, bool u8) {
 }
 
 // warp-specialised kernel: two U' row buffers and two F row buffers
+size_t smem_layout_ws2(KParams& P, bool u8) {
+  size_t off = (sizeof(int) * 2 * P.ns * 4 * (size_t)P.nk * W2_UP + 15) / 16 * 16;
+  P.f_off = (int)off;
+  P.l_off = (int)off;
+  if (u8) off += 256 * (sizeof(float2) + sizeof(double2));
+  return off;
+}
+
 size_t smem_layout_ws(KParams& P, int MAXK, bool u8) {
   auto up16 = [](size_t v) { return (v + 15) / 16 * 16; };
   size_t off = up16(sizeof(int) * 2 * P.ns * 4 * (size_t)P.nk * (WS_V + 2));
@@ -1179,9 +1390,21 @@ size_t smem_layout_ws(KParams& P, int MAXK, bool u8) {
 }
 
 template <int MAXK, int FORM, bool U8, int NT, bool CONSEC, bool FULL = false, bool MULTI = false>
-cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim3 grid, cudaStream_t st, bool wsk) {
+cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim3 grid, cudaStream_t st, int kern) {
   if constexpr (NT == WS_V && FORM != 4) {
-    if (wsk) {
+    if (kern == KERN_WS2) {
+      if constexpr (!MULTI && FORM != 5) {
+        auto kfn = bf_ws2_kernel<MAXK, FORM, U8, CONSEC, FULL>;
+        const size_t smem = smem_layout_ws2(P, U8);
+        if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+        cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kfn<<<grid, W2_THREADS, smem, st>>>(P, in, out, ws);
+        return cudaGetLastError();
+      }
+      return cudaErrorInvalidConfiguration;
+    }
+    if (kern == KERN_WS) {
       auto kfn = bf_ws_kernel<MAXK, FORM, U8, CONSEC, FULL, MULTI>;
       const size_t smem = smem_layout_ws(P, MAXK, U8);
       if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
@@ -1202,26 +1425,26 @@ cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim
 
 template <int MAXK, int FORM, bool U8, int NT>
 cudaError_t dispatch_consec(bool consec, const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid,
-                            cudaStream_t st, bool wsk) {
+                            cudaStream_t st, int kern) {
   if (P.nplans > 1) {   // Case 1 multi-plan combine: its own instantiation (register pressure)
     if constexpr (FORM == 1 || FORM == 2) {
-      return consec ? launch_one<MAXK, FORM, U8, NT, true, false, true>(P, in, out, ws, grid, st, wsk)
-                    : launch_one<MAXK, FORM, U8, NT, false, false, true>(P, in, out, ws, grid, st, wsk);
+      return consec ? launch_one<MAXK, FORM, U8, NT, true, false, true>(P, in, out, ws, grid, st, kern)
+                    : launch_one<MAXK, FORM, U8, NT, false, false, true>(P, in, out, ws, grid, st, kern);
     }
     return cudaErrorInvalidConfiguration;
   }
-  if (consec && P.nk == MAXK) return launch_one<MAXK, FORM, U8, NT, true, true>(P, in, out, ws, grid, st, wsk);
-  if (consec) return launch_one<MAXK, FORM, U8, NT, true>(P, in, out, ws, grid, st, wsk);
-  return launch_one<MAXK, FORM, U8, NT, false>(P, in, out, ws, grid, st, wsk);
+  if (consec && P.nk == MAXK) return launch_one<MAXK, FORM, U8, NT, true, true>(P, in, out, ws, grid, st, kern);
+  if (consec) return launch_one<MAXK, FORM, U8, NT, true>(P, in, out, ws, grid, st, kern);
+  return launch_one<MAXK, FORM, U8, NT, false>(P, in, out, ws, grid, st, kern);
 }
 
 template <int MAXK, bool U8, int NT>
 cudaError_t dispatch_form(int form, bool consec, const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid,
-                          cudaStream_t st, bool wsk) {
+                          cudaStream_t st, int kern) {
   switch (form) {
-    case 1: return dispatch_consec<MAXK, 1, U8, NT>(consec, P, in, out, ws, grid, st, wsk);
-    case 2: return dispatch_consec<MAXK, 2, U8, NT>(consec, P, in, out, ws, grid, st, wsk);
-    case 4: return launch_one<MAXK, 4, U8, NT, false>(P, in, out, ws, grid, st, false);
+    case 1: return dispatch_consec<MAXK, 1, U8, NT>(consec, P, in, out, ws, grid, st, kern);
+    case 2: return dispatch_consec<MAXK, 2, U8, NT>(consec, P, in, out, ws, grid, st, kern);
+    case 4: return launch_one<MAXK, 4, U8, NT, false>(P, in, out, ws, grid, st, KERN_BAND);
     default: break;
   }
   return cudaErrorInvalidConfiguration;
@@ -1229,7 +1452,7 @@ cudaError_t dispatch_form(int form, bool consec, const KParams& P, const void* i
 
 struct Shape {
   int NT, MAXK;
-  bool wsk;   // warp-specialised kernel (NT = 256, at most 2 boxes per axis)
+  int kern;   // KERN_BAND; KERN_WS / KERN_WS2 (warp-specialised, NT = 256 class, at most 2 box streams)
   int form;   // Form<FORM>: 1, 2, 4 separable with that many boxes; 5 rank 2
 };
 
@@ -1237,7 +1460,7 @@ struct Shape {
 // possible), MAXK terms per pass (the vertical state is NS * 4 * MAXK registers per thread) and
 // the spatial form. Returns NT = 0 if the plan has no GPU form.
 Shape plan_shape(const bf_plan* p, int& rlo, int& rhi) {
-  Shape sh{0, 0, false, 0};
+  Shape sh{0, 0, KERN_BAND, 0};
   rlo = rhi = 0;
   if (p->ns < 1 || p->ns > 2) return sh;
   int nbx = 0, nby = p->snby[0];
@@ -1265,16 +1488,20 @@ Shape plan_shape(const bf_plan* p, int& rlo, int& rhi) {
   if (halo <= 128) {
     sh.NT = 256;
     sh.MAXK = (nk <= 8 || p->ns == 2) ? 8 : 16;
-    sh.wsk = sh.form != 4;
+    // kernel 2b for the separable forms; the rank-2 form's vertical state (NS = 2 taps sets)
+    // needs more than 2b's 112 V registers, it keeps kernel 2
+    sh.kern = sh.form == 4 ? KERN_BAND : (sh.form == 5 ? KERN_WS : KERN_WS2);
   } else {
     sh.NT = 512;
     sh.MAXK = 8;
-    sh.wsk = false;
+    sh.kern = KERN_BAND;
   }
   if (const char* e = std::getenv("BF_MAXK")) sh.MAXK = (std::atoi(e) <= 8 || p->ns == 2) ? 8 : 16;   // tuning hook
   if (const char* e = std::getenv("BF_KERNEL")) {   // tuning hook: force one kernel
-    if (std::strcmp(e, "band") == 0) sh.wsk = false;
-    if (std::strcmp(e, "ws") == 0) sh.wsk = (sh.NT == 256 && sh.form != 4);
+    if (std::strcmp(e, "band") == 0) sh.kern = KERN_BAND;
+    if (std::strcmp(e, "ws") == 0) sh.kern = (sh.NT == 256 && sh.form != 4) ? KERN_WS : KERN_BAND;
+    if (std::strcmp(e, "ws2") == 0) sh.kern = (sh.NT == 256 && sh.form != 4) ? KERN_WS2 : KERN_BAND;
+    if (std::strcmp(e, "ws2") == 0 && sh.form == 5) sh.kern = KERN_WS;
   }
   if (sh.NT == 512) sh.MAXK = 8;
   if (halo + 32 > sh.NT) sh.NT = 0;
@@ -1286,18 +1513,19 @@ cudaError_t dispatch(const Shape& sh, bool consec, const KParams& P, const void*
                      dim3 grid, cudaStream_t st) {
   if (sh.form == 5) {   // rank 2: NS * 4 * 8 = 64 state registers, NT = 256 only
     if (sh.NT != 256 || sh.MAXK != 8) return cudaErrorInvalidConfiguration;
-    return dispatch_consec<8, 5, U8, 256>(consec, P, in, out, ws, grid, st, sh.wsk);
+    return dispatch_consec<8, 5, U8, 256>(consec, P, in, out, ws, grid, st, sh.kern);
   }
-  if (sh.NT == 256 && sh.MAXK == 8) return dispatch_form<8, U8, 256>(sh.form, consec, P, in, out, ws, grid, st, sh.wsk);
+  if (sh.NT == 256 && sh.MAXK == 8) return dispatch_form<8, U8, 256>(sh.form, consec, P, in, out, ws, grid, st, sh.kern);
   if (sh.NT == 256 && sh.MAXK == 16)
-    return dispatch_form<16, U8, 256>(sh.form, consec, P, in, out, ws, grid, st, sh.wsk);
-  if (sh.NT == 512 && sh.MAXK == 8) return dispatch_form<8, U8, 512>(sh.form, consec, P, in, out, ws, grid, st, false);
+    return dispatch_form<16, U8, 256>(sh.form, consec, P, in, out, ws, grid, st, sh.kern);
+  if (sh.NT == 512 && sh.MAXK == 8) return dispatch_form<8, U8, 512>(sh.form, consec, P, in, out, ws, grid, st, KERN_BAND);
   return cudaErrorInvalidConfiguration;
 }
 
 // The literal-window path (kernel 3): u8 input, levels 0..255 (D = 255), separable plans with
 // at most two boxes per axis whose halo fits the 128-column strip.
-bf_status run_literal(const bf_plan* p, const void* d_in, float* d_out, int n_frames, int H, int W, cudaStream_t st) {
+bf_status run_literal(const bf_plan* p, const void* d_in, float* d_out, int n_frames, int H, int W, cudaStream_t st,
+                      bf_launch_config* dry) {
   if (p->input_dtype != BF_IN_U8 || p->D != 255.0 || p->ns != 1 || p->snbx[0] > 2 || p->snby[0] > 2)
     return BF_ERR_UNSUPPORTED;
   LParams L;
@@ -1361,10 +1589,14 @@ bf_status run_literal(const bf_plan* p, const void* d_in, float* d_out, int n_fr
   L.TH = (H + best_nb - 1) / best_nb;
   if (const char* e = std::getenv("BF_TH")) L.TH = std::max(1, std::min(H, std::atoi(e)));   // test hook
   best_nb = (H + L.TH - 1) / L.TH;
+  const size_t smem = sizeof(int) * (256 * (LIT_NT + 1) + 512);
+  if (dry) {
+    *dry = bf_launch_config{1, "bf_literal_kernel", LIT_NT, nstrips, best_nb, n_frames, L.TW, L.TH, smem};
+    return BF_OK;
+  }
   int* dk = nullptr;   // the 2 KB table travels through a stream-ordered allocation
   if (cudaMallocAsync(&dk, sizeof(hk), st) != cudaSuccess) return BF_ERR_CUDA;
   cudaError_t err = cudaMemcpyAsync(dk, hk, sizeof(hk), cudaMemcpyHostToDevice, st);
-  const size_t smem = sizeof(int) * (256 * (LIT_NT + 1) + 512);
   if (err == cudaSuccess)
     err = cudaFuncSetAttribute(bf_literal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err == cudaSuccess) {
@@ -1391,9 +1623,10 @@ bool same_channels(const bf_plan* a, const bf_plan* b) {
   return true;
 }
 
+// dry != nullptr: describe the launches (bf_apply_config) instead of enqueueing them
 bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, float* d_out, int n_frames, int H,
-                     int W, cudaStream_t st) {
-  if (!plans || nplans < 1 || nplans > MAXP || !d_in || !d_out || H <= 0 || W <= 0 || n_frames <= 0)
+                     int W, cudaStream_t st, bf_launch_config* dry = nullptr) {
+  if (!plans || nplans < 1 || nplans > MAXP || (!dry && (!d_in || !d_out)) || H <= 0 || W <= 0 || n_frames <= 0)
     return BF_ERR_INVALID_ARG;
   for (int q = 0; q < nplans; ++q)
     if (!plans[q]) return BF_ERR_INVALID_ARG;
@@ -1418,15 +1651,34 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
   const bf_plan* p = &merged;
   if (p->literal) {
     if (nplans != 1) return BF_ERR_UNSUPPORTED;
-    return run_literal(p, d_in, d_out, n_frames, H, W, st);
+    return run_literal(p, d_in, d_out, n_frames, H, W, st, dry);
   }
   if ((long long)H * W > (1LL << 40) / n_frames) return BF_ERR_INVALID_ARG;
-  if ((const void*)d_out == d_in) return BF_ERR_INVALID_ARG;
+  if (!dry && (const void*)d_out == d_in) return BF_ERR_INVALID_ARG;
   int rlo, rhi;
   Shape sh = plan_shape(p, rlo, rhi);
   if (sh.NT == 0) return BF_ERR_UNSUPPORTED;
-  const int TW = sh.NT - (rlo + rhi);
   const int ns = p->ns;
+  // paired-load layout of the horizontal boxes (warp-specialised kernel): every box symmetric
+  // [-r_b, r_b] (odd width), at most two boxes in all, box 0 the widest (leave stream even)
+  int wpar = -1;
+  {
+    int m = 0, r0 = -1, r1 = -1;
+    bool ok = true;
+    for (int t = 0; t < ns; ++t)
+      for (int b = 0; b < p->snbx[t]; ++b) {
+        if (p->slox[t][b] != -p->shix[t][b]) ok = false;
+        if (m == 0) r0 = p->shix[t][b];
+        else r1 = p->shix[t][b];
+        ++m;
+      }
+    if (ok && m <= 2 && r0 == rlo && (m == 1 || r1 <= r0)) wpar = (m == 2) ? ((r0 - r1) & 1) : 0;
+  }
+  if (nplans > 1) sh.kern = KERN_BAND;            // Case 1 multi-plan combine: band kernel (measured faster)
+  if (sh.kern == KERN_WS && wpar < 0) sh.kern = KERN_BAND;
+  if ((4 * std::min(sh.MAXK, p->n_k) + 31) / 32 > 2) sh.kern = KERN_BAND;   // two scan warps
+  const int halo = rlo + rhi;
+  const int TW = (sh.kern == KERN_WS2) ? std::min(W2_H, W2_V - halo) : sh.NT - halo;
 
   KParams P;
   std::memset(&P, 0, sizeof(P));
@@ -1467,30 +1719,31 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
     }
     ubound = std::max(ubound, ub);
   }
+  // ---- U' = U >> ush: every horizontal box sum H of U' fits int32
   int nxmax = 1;
   for (int t = 0; t < ns; ++t)
     for (int b = 0; b < p->snbx[t]; ++b) nxmax = std::max(nxmax, p->shix[t][b] - p->slox[t][b] + 1);
   P.ush = 0;
   while ((ubound / std::ldexp(1.0, P.ush) + 1.0) * nxmax >= 2147483000.0) ++P.ush;
   P.urnd = P.ush > 0 ? (1 << (P.ush - 1)) : 0;
-  // ---- horizontal: integer weights, F narrowed to int32
-  double wxmax = 0.0;
+  const double uprime = ubound / std::ldexp(1.0, P.ush) + 1.0;
+  // ---- horizontal: integer weights ax = round(wx / max|wx| * 2^abits), F = sum mulhi(H, ax)
+  //      (one IMAD.HI per box; each high word truncates, so |F - exact| < ns * nbx) fits int32
+  double wxmax = 0.0, rw = 0.0;
   for (int t = 0; t < ns; ++t)
     for (int b = 0; b < p->snbx[t]; ++b) wxmax = std::max(wxmax, std::fabs(p->swx[t][b]));
-  const double uprime = ubound / std::ldexp(1.0, P.ush) + 1.0;
-  double fb = 0.0;
+  for (int t = 0; t < ns; ++t)
+    for (int b = 0; b < p->snbx[t]; ++b) rw += std::fabs(p->swx[t][b]) / wxmax * (p->shix[t][b] - p->slox[t][b] + 1);
+  int abits = ABITS;
+  while (abits > 16 && uprime * rw * std::ldexp(1.0, abits - 32) + 8.0 >= 2147483000.0) --abits;
   for (int t = 0; t < ns; ++t) {
     P.nbx[t] = p->snbx[t];
     for (int b = 0; b < p->snbx[t]; ++b) {
       P.hlo[t][b] = p->slox[t][b];
       P.hhi[t][b] = p->shix[t][b];
-      P.ax[t][b] = (int)std::lround(std::ldexp(p->swx[t][b] / wxmax, ABITS));
-      fb += std::fabs((double)P.ax[t][b]) * uprime * (p->shix[t][b] - p->slox[t][b] + 1);
+      P.ax[t][b] = (int)std::lround(std::ldexp(p->swx[t][b] / wxmax, abits));
     }
   }
-  P.fsh = 0;
-  while (fb / std::ldexp(1.0, P.fsh) >= 2147483000.0) ++P.fsh;
-  P.frnd = P.fsh > 0 ? (1LL << (P.fsh - 1)) : 0;
   // ---- combine weights a_k * 2^wbits: |W| < 2^31 and |num|, |den| < 2^62
   double asum = 0.0, amax = 0.0;
   for (int q = 0; q < nplans; ++q) {
@@ -1512,35 +1765,18 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
 
   const int passes = (p->n_k + sh.MAXK - 1) / sh.MAXK;
   if (nplans > 1 && passes > 1) return BF_ERR_UNSUPPORTED;   // shared channels must fit one pass
-  // paired-load layout of the horizontal boxes (warp-specialised kernel): every box symmetric
-  // [-r_b, r_b] (odd width), at most two boxes in all, box 0 the widest (leave stream even)
-  int wpar = -1;
-  {
-    int m = 0, r0 = -1, r1 = -1;
-    bool ok = true;
-    for (int t = 0; t < ns; ++t)
-      for (int b = 0; b < p->snbx[t]; ++b) {
-        if (p->slox[t][b] != -p->shix[t][b]) ok = false;
-        if (m == 0) r0 = p->shix[t][b];
-        else r1 = p->shix[t][b];
-        ++m;
-      }
-    if (ok && m <= 2 && r0 == rlo && (m == 1 || r1 <= r0)) wpar = (m == 2) ? ((r0 - r1) & 1) : 0;
-  }
-  if (wpar < 0) sh.wsk = false;
-  if ((4 * std::min(sh.MAXK, p->n_k) + 31) / 32 > 2) sh.wsk = false;   // two scan warps
   P.nplans = nplans;
   P.plan_stride = (long long)H * W;
-  if (sh.wsk) {   // the double-buffered rows must fit the 227 KB of shared memory
+  if (sh.kern == KERN_WS) {   // the double-buffered rows must fit the 227 KB of shared memory
     KParams Q = P;
     Q.nk = std::min(sh.MAXK, p->n_k);
-    if (smem_layout_ws(Q, sh.MAXK, p->input_dtype == BF_IN_U8) > 227 * 1024) sh.wsk = false;
+    if (smem_layout_ws(Q, sh.MAXK, p->input_dtype == BF_IN_U8) > 227 * 1024) sh.kern = KERN_BAND;
   }
   const int nstrips = (W + TW - 1) / TW;
   // ---- band height: CTAs in whole waves of the resident slots, init (vmax - vmin + 1 rows)
   //      amortised over the band
   const int nsm = sm_count();
-  const int slots = nsm * ((sh.NT > 256 || sh.wsk) ? 1 : 2);
+  const int slots = nsm * ((sh.NT > 256 || sh.kern != KERN_BAND) ? 1 : 2);
   const int ry = P.vmax - P.vmin + 1;
   long long best_cost = -1;
   int best_nb = 1;
@@ -1559,6 +1795,27 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
   if (const char* e = std::getenv("BF_TH")) P.TH = std::max(1, std::min(H, std::atoi(e)));   // test hook
   best_nb = (H + P.TH - 1) / P.TH;
 
+  if (dry) {
+    KParams Q = P;
+    Q.nk = std::min(sh.MAXK, p->n_k);
+    const bool u8 = (p->input_dtype == BF_IN_U8);
+    size_t smem = 0;
+    const char* name = "bf_band_kernel";
+    int threads = sh.NT;
+    if (sh.kern == KERN_WS2) {
+      smem = smem_layout_ws2(Q, u8);
+      name = "bf_ws2_kernel";
+      threads = W2_THREADS;
+    } else if (sh.kern == KERN_WS) {
+      smem = smem_layout_ws(Q, sh.MAXK, u8);
+      name = "bf_ws_kernel";
+      threads = WS_THREADS;
+    } else {
+      smem = smem_layout(Q, sh.NT, sh.MAXK, u8);
+    }
+    *dry = bf_launch_config{passes, name, threads, nstrips, best_nb, n_frames, TW, P.TH, smem};
+    return BF_OK;
+  }
   longlong2* ws = nullptr;
   if (passes > 1) {
     if (cudaMallocAsync(&ws, sizeof(longlong2) * (size_t)H * W * n_frames, st) != cudaSuccess) return BF_ERR_CUDA;
@@ -1588,16 +1845,17 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
       }
     }
     // walker segments: ngrp * nseg warps; long segments amortise the initial window sums
-    const int max_tasks = sh.wsk ? WS_H / 32 : sh.NT / 32;   // (prefix form: WS_F / 32, set below)
+    const int max_tasks = sh.kern == KERN_WS ? WS_H / 32 : sh.NT / 32;   // (prefix form: WS_F / 32, set below)
     int nseg = std::max(1, max_tasks / P.ngrp);
-    const int min_len = sh.wsk ? 24 : std::max(32, 2 * (rlo + rhi + 1) / 3);
+    const int min_len = sh.kern == KERN_WS ? 24 : std::max(32, 2 * (rlo + rhi + 1) / 3);
     while (nseg > 1 && (TW + nseg - 1) / nseg < min_len) --nseg;
     if (const char* e = std::getenv("BF_NSEG")) nseg = std::max(1, std::min(max_tasks / P.ngrp, std::atoi(e)));  // tuning hook
     P.nseg = nseg;
     P.seglen = (TW + nseg - 1) / nseg;
     P.seglen += P.seglen & 1;   // even segment starts (paired loads)
-    P.wpar = sh.wsk ? wpar : -1;
-    if (sh.wsk) {   // F warps of the warp-specialised kernel: (WS_F / 32) / ngrp segments per group
+    P.wpar = sh.kern == KERN_WS ? wpar : -1;
+    P.wv = (TW + halo + 7) & ~7;
+    if (sh.kern == KERN_WS) {   // F warps of the warp-specialised kernel: (WS_F / 32) / ngrp segments per group
       P.nseg = std::max(1, (WS_F / 32) / P.ngrp);
       P.seglen = (TW + P.nseg - 1) / P.nseg;
       P.seglen += P.seglen & 1;
@@ -1638,6 +1896,11 @@ extern "C" bf_status bf_apply_launches(const bf_plan* p, int H, int W, int* n) {
   if (sh.NT == 0) return BF_ERR_UNSUPPORTED;
   *n = (p->n_k + sh.MAXK - 1) / sh.MAXK;
   return BF_OK;
+}
+
+extern "C" bf_status bf_apply_config(const bf_plan* plan, int n_frames, int H, int W, bf_launch_config* cfg) {
+  if (!plan || !cfg || H <= 0 || W <= 0 || n_frames <= 0) return BF_ERR_INVALID_ARG;
+  return run_filter(&plan, 1, nullptr, nullptr, n_frames, H, W, nullptr, cfg);
 }
 
 extern "C" bf_status bf_apply(const bf_plan* plan, const void* d_in, float* d_out, int H, int W, bf_stream stream) {

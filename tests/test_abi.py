@@ -30,7 +30,8 @@ def header_functions():
 def test_header_declares_expected_api():
     assert header_functions() == sorted(["bf_plan_options_default", "bf_plan_create", "bf_plan_destroy",
                                          "bf_plan_get_info", "bf_apply", "bf_apply_batched", "bf_apply_host",
-                                         "bf_apply_launches", "bf_apply_multi", "bf_status_string", "bf_version"])
+                                         "bf_apply_config", "bf_apply_launches", "bf_apply_multi",
+                                         "bf_status_string", "bf_version"])
 
 
 def test_library_exports_every_declared_symbol(bfmod):
@@ -134,6 +135,44 @@ def test_launch_count_query(bfmod):
     n = C.c_int(7)
     assert L.bf_apply_launches(None, 4, 4, C.byref(n)) == bfmod.BF_ERR_INVALID_ARG
     assert L.bf_apply_launches(plan.handle, 0, 4, C.byref(n)) == bfmod.BF_ERR_INVALID_ARG
+
+
+def test_launch_config_query(bfmod, monkeypatch):
+    """bf_apply_config describes the launches without device work: the fused warp-specialised
+    kernel (768 threads, TW = 384 - halo output columns) for the separable N_s = 9 plans, the
+    band kernel for cfg4's r = 192 halo (3 passes), the literal kernel for range_window='literal';
+    BF_KERNEL forces a kernel; the grid covers the image."""
+    import ctypes as C
+    for cfg, kern, launches in (("cfg2", "bf_ws2_kernel", 1), ("cfg1", "bf_ws2_kernel", 1),
+                                ("cfg4", "bf_band_kernel", 3)):
+        spec = CONFIGS[cfg]
+        p = config_params(spec)
+        plan = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"],
+                          sigma_r=p["sigma_r"], radius=p["radius"], n_terms=p["n_terms"],
+                          intensity_max=p["intensity_max"])
+        c = bfmod.config(plan, spec.H, spec.W)
+        assert c["kernel"] == kern and c["launches"] == launches == bfmod.launches(plan, spec.H, spec.W), cfg
+        tw, th = c["tile"]
+        gx, gy, gz = c["grid"]
+        assert gx * tw >= spec.W > (gx - 1) * tw and gy * th >= spec.H > (gy - 1) * th and gz == 1
+        assert c["smem_bytes"] <= 227 * 1024
+        if kern == "bf_ws2_kernel":
+            halo = 2 * p["radius"]
+            assert c["threads_per_cta"] == 768 and tw == min(320, 384 - halo)
+    spec = CONFIGS["cfg2"]
+    p = config_params(spec)
+    plan = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"], sigma_r=p["sigma_r"],
+                      radius=p["radius"], n_terms=p["n_terms"], intensity_max=p["intensity_max"])
+    for k, name, threads in (("band", "bf_band_kernel", 256), ("ws", "bf_ws_kernel", 640)):
+        monkeypatch.setenv("BF_KERNEL", k)
+        c = bfmod.config(plan, 333, 361)
+        assert (c["kernel"], c["threads_per_cta"], c["tile"][0]) == (name, threads, 256 - 2 * p["radius"])
+    monkeypatch.delenv("BF_KERNEL")
+    lit = bfmod.Plan(range_window="literal", input_dtype="u8", radius=10, n_terms=4)
+    assert bfmod.config(lit, 100, 100)["kernel"] == "bf_literal_kernel"
+    c = bfmod.LaunchConfig()
+    assert bfmod.lib().bf_apply_config(None, 1, 4, 4, C.byref(c)) == bfmod.BF_ERR_INVALID_ARG
+    assert bfmod.lib().bf_apply_config(plan.handle, 0, 4, 4, C.byref(c)) == bfmod.BF_ERR_INVALID_ARG
 
 
 def test_spatial_rank_of_the_gpu_form(bfmod):

@@ -200,19 +200,20 @@ def test_rank2_three_box_plan(gpu, cfg, H, W, monkeypatch):
 @pytest.mark.parametrize("cfg,H,W", [("cfg0", 256, 256), ("cfg1", 150, 347), ("cfg2", 333, 361), ("cfg3", 211, 333),
                                      ("cfg1", 3, 500), ("cfg2", 97, 161)])
 def test_kernels_agree_bitwise(gpu, cfg, H, W, monkeypatch):
-    """The warp-specialised kernel (named-barrier pipeline, BF_KERNEL=ws) and the barrier-interval
-    kernel (BF_KERNEL=band) perform the same exact integer arithmetic with different schedules and
+    """The warp-specialised kernels (named-barrier pipelines, BF_KERNEL=ws / ws2) and the
+    barrier-interval kernel (BF_KERNEL=band) perform the same exact integer arithmetic with different schedules and
     walker segmentations: their outputs must be bitwise equal (a synchronisation race would show)."""
     pkg, torch = gpu
     spec = CONFIGS[cfg]
     img = config_input(spec, H=H, W=W)
     gp, op = make_plans(pkg, config_params(spec), img.dtype)
     outs = {}
-    for k in ("band", "ws"):
+    for k in ("band", "ws", "ws2"):
         monkeypatch.setenv("BF_KERNEL", k)
         outs[k] = run_gpu(pkg, torch, gp, img)
     assert np.array_equal(outs["band"], outs["ws"])
-    assert_parity(outs["ws"], bf.bf_box(img, op), spec.intensity_max, cfg)
+    assert np.array_equal(outs["band"], outs["ws2"])
+    assert_parity(outs["ws2"], bf.bf_box(img, op), spec.intensity_max, cfg)
 
 
 def test_multi_plan_case1_shared_channels(gpu):
@@ -242,7 +243,7 @@ def test_multi_plan_case1_shared_channels(gpu):
 
 @pytest.mark.parametrize("cfg,H,W", [("cfg0", 300, 256), ("cfg2", 260, 300), ("cfg3", 200, 240),
                                      ("cfg4", 420, 300)])
-@pytest.mark.parametrize("kernel", ["band", "ws"])
+@pytest.mark.parametrize("kernel", ["band", "ws", "ws2"])
 def test_sliding_sums_are_exact(gpu, cfg, H, W, kernel, monkeypatch):
     """The vertical state slides by adding the quantised enter taps and subtracting the leave
     taps, which must cancel EXACTLY (the leave tap regenerates bit for bit what the enter tap, or

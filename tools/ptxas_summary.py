@@ -12,13 +12,13 @@ for line in (r.stdout + r.stderr).splitlines():
     m = re.search(r"Compiling entry function '(\S+)'", line)
     if m:
         name = m.group(1)
-        k = re.search(r"kernelI(.*)EEEv", name)
-        name = k.group(1) if k else name
+        k = re.search(r"(bf_\w+?_kernel)I(.*)EEEv", name)
+        name = (k.group(1) + "<" + re.sub(r"L[ib](\d+)E", r"\1,", k.group(2) + "E").rstrip(",") + ">") if k else name
     m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", line)
     if m:
         spill = f"spill st {m.group(1)} ld {m.group(2)}"
     m = re.search(r"Used (\d+) registers", line)
     if m and name:
-        print(f"{name:40s} regs {m.group(1):>4s}  {spill}")
+        print(f"{name:48s} regs {m.group(1):>4s}  {spill}")
     if "error" in line:
         print(line)
