@@ -10,10 +10,10 @@ streams; every step of the filter runs in the library's host fitter and sm_100a 
 """
 from __future__ import annotations
 
-from ._bf import (BFError, Plan, apply, apply_batched, apply_host, apply_multi, launches, lib, version)
+from ._bf import (BFError, Plan, apply, apply_batched, apply_host, apply_multi, config, launches, lib, version)
 
 __all__ = ["BFError", "Plan", "apply", "apply_batched", "apply_host", "apply_multi", "bilateral_filter",
-           "bilateral_filter_multi", "launches", "lib", "version"]
+           "bilateral_filter_multi", "config", "launches", "lib", "version"]
 
 
 def _check_tensor(t, plan):

@@ -1678,7 +1678,7 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
   if (sh.kern == KERN_WS && wpar < 0) sh.kern = KERN_BAND;
   if ((4 * std::min(sh.MAXK, p->n_k) + 31) / 32 > 2) sh.kern = KERN_BAND;   // two scan warps
   const int halo = rlo + rhi;
-  const int TW = (sh.kern == KERN_WS2) ? std::min(W2_H, W2_V - halo) : sh.NT - halo;
+  int TW = (sh.kern == KERN_WS2) ? std::min(W2_H, W2_V - halo) : sh.NT - halo;   // widest strip
 
   KParams P;
   std::memset(&P, 0, sizeof(P));
@@ -1772,25 +1772,43 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
     Q.nk = std::min(sh.MAXK, p->n_k);
     if (smem_layout_ws(Q, sh.MAXK, p->input_dtype == BF_IN_U8) > 227 * 1024) sh.kern = KERN_BAND;
   }
-  const int nstrips = (W + TW - 1) / TW;
-  // ---- band height: CTAs in whole waves of the resident slots, init (vmax - vmin + 1 rows)
-  //      amortised over the band
+  // ---- tile: band height TH (kernel 2b: and strip width TW) minimising the modelled time: CTAs
+  //      in whole waves of the resident slots, each TH rows at the row cost plus the initial
+  //      vertical sum over vmax - vmin + 1 rows. Kernel 2b's row time: warp-instructions per
+  //      role (ncu, cfg2: V 694 per 32 extended columns, FH 942 per 32 outputs, S ~4 per column;
+  //      V init 373 per 32 columns) at the measured ~0.55 IPC per SM sub-partition, but never
+  //      below the ~6000 cycles one warp's dependent chain takes (measured at 128-column strips):
+  //      a narrower strip can fill the 148 SMs better.
   const int nsm = sm_count();
   const int slots = nsm * ((sh.NT > 256 || sh.kern != KERN_BAND) ? 1 : 2);
   const int ry = P.vmax - P.vmin + 1;
-  long long best_cost = -1;
-  int best_nb = 1;
-  for (int nb = 1; nb <= H; ++nb) {
-    const int TH = (H + nb - 1) / nb;
-    if (nb > 1 && TH < 16) break;
-    const long long ctas = (long long)nstrips * nb * n_frames;
-    const long long waves = (ctas + slots - 1) / slots;
-    const long long cost = waves * (4LL * TH + ry);
-    if (best_cost < 0 || cost < best_cost) {
-      best_cost = cost;
-      best_nb = nb;
+  double best_cost = -1.0;
+  int best_nb = 1, best_tw = TW;
+  for (int tw = TW; tw >= 1; tw = (tw % 32) ? tw - tw % 32 : tw - 32) {
+    if (tw != TW && (sh.kern != KERN_WS2 || tw < 128)) break;
+    double row = 4.0, init = 1.0;
+    if (sh.kern == KERN_WS2) {
+      const int wv = (tw + halo + 7) & ~7;
+      row = std::max(6000.0, (694.0 * ((wv + 31) / 32) + 942.0 * ((tw + 31) / 32) + 4.0 * wv) / (4 * 0.55));
+      init = std::max(1500.0, 373.0 * ((wv + 31) / 32) / (4 * 0.55));
+    }
+    const long long strips = (W + tw - 1) / tw;
+    for (int nb = 1; nb <= H; ++nb) {
+      const int TH = (H + nb - 1) / nb;
+      if (nb > 1 && TH < 16) break;
+      const long long ctas = strips * nb * n_frames;
+      const long long waves = (ctas + slots - 1) / slots;
+      const double cost = (double)waves * (TH * row + ry * init);
+      if (best_cost < 0 || cost < best_cost * (1.0 - 1e-9)) {
+        best_cost = cost;
+        best_nb = nb;
+        best_tw = tw;
+      }
     }
   }
+  TW = best_tw;
+  P.TW = TW;
+  const int nstrips = (W + TW - 1) / TW;
   P.TH = (H + best_nb - 1) / best_nb;
   if (const char* e = std::getenv("BF_TH")) P.TH = std::max(1, std::min(H, std::atoi(e)));   // test hook
   best_nb = (H + P.TH - 1) / P.TH;
