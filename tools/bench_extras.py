@@ -75,7 +75,7 @@ def main():
         sp = CONFIGS[cfg]
         im = torch.from_numpy(config_input(sp)).cuda()
         p = plan_for(sp)
-        for k in ("band", "ws"):
+        for k in ("band", "ws", "ws2"):
             os.environ["BF_KERNEL"] = k
             t = timed(lambda: pkg.bilateral_filter(p, im))
             print(f"{cfg} kernel={k}: {t:.3f} ms")
