@@ -1034,9 +1034,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 // ------------------------------------------------------------------ kernel 2b: fused box-difference + combine
 // Three roles; the F row buffer of kernel 2 is gone, which pays for 384 extended columns
 // (TW = min(320, 384 - halo) outputs: halo overhead 1.33x instead of 1.6x at r = 48):
-//   warps 0-11   V: one thread per extended column, writes U'(y) group by group (as kernel 2)
-//   warps 12-13  S: warp g turns group g's U' rows into exclusive prefix rows Q in place
-//   warps 14-23  FH: one thread per output pixel: for every channel slot of group g,
+//   warps 12-23  V: one thread per extended column, writes U'(y) group by group (as kernel 2)
+//   warps 10-11  S: warp g turns group g's U' rows into exclusive prefix rows Q in place
+//   warps 0-9    FH: one thread per output pixel: for every channel slot of group g,
 //                F = sum_b mulhi(Q[x + hi_b + 1] - Q[x + lo_b], ax_b) (lanes = consecutive
 //                x: conflict-free), accumulated straight into the exact int64 num / den with the
 //                pixel's fp64 combine weights; then out = D num / den
@@ -1044,6 +1044,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 //   U_FULL(b,g) 0-3   V arrive, S_g sync        U_EMPTY(b,g) 4-7  FH arrive, V sync
 //   Q_FULL(b,g) 8-11  S_g arrive, FH sync       (b = row parity, g = channel group)
 constexpr int W2_V = 384, W2_S = 64, W2_H = 320, W2_THREADS = W2_V + W2_S + W2_H;
+// thread ranges of the roles: FH first (warps 0-9), then S (10-11), then V (12-23) — the warp
+// schedulers favour older (lower) warps, and FH is the role on the critical path
+constexpr int W2_H0 = 0, W2_S0 = W2_H, W2_V0 = W2_H + W2_S;
 constexpr int W2_UP = W2_V + 4;   // == 4 mod 32: conflict-free LDS.128 / STS.128 with lanes = channels
 
 // Exclusive prefix of one U' row in place, 8 columns per step (two 16-byte loads / stores, one
@@ -1113,12 +1116,13 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   fill_luts<U8>(P, lut, lut64, tid, W2_THREADS);
   __syncthreads();
 
-  if (tid < W2_V) {
+  if (tid >= W2_V0) {
     // ------------------------------------------------------------ V role
     asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
-    const int col = x0 - P.rlo_x + tid;
-    const bool colok = (col >= 0) & (col < P.W) & (tid < wv);
-    const bool vwork = (tid & ~31) < wv;          // warps wholly past the scanned columns only sync
+    const int vt = tid - W2_V0;                   // extended column
+    const int col = x0 - P.rlo_x + vt;
+    const bool colok = (col >= 0) & (col < P.W) & (vt < wv);
+    const bool vwork = (vt & ~31) < wv;           // warps wholly past the scanned columns only sync
     int U[NS * 4 * MAXK];
     if (vwork) v_init<MAXK, NB, NS, U8, CONSEC, FULL>(P, in, lut, fbase, col, colok, y0, U);
     float Ipre[NB][2];
@@ -1134,7 +1138,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
           Icur[bb][1] = Ipre[bb][1];
         }
         if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col, colok, y + 1, Ipre);
-        v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + b * ustride + tid, &hook);
+        v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP>(P, lut, colok, y, Icur, U, Ubuf + b * ustride + vt, &hook);
       } else {
         for (int g = 0; g < ngrp; ++g) {
           hook.begin(g);
@@ -1145,10 +1149,10 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
     // drain: the FH warps' last releases
     for (int y = max(y0, yend - 2); y < yend; ++y)
       for (int g = 0; g < ngrp; ++g) bar_sync(BAR_U_EMPTY + 2 * ((y - y0) & 1) + g, n_uempty);
-  } else if (tid < W2_V + W2_S) {
+  } else if (tid >= W2_S0) {
     // ------------------------------------------------------------ S role: prefix scans
     asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
-    const int g = (tid - W2_V) >> 5;
+    const int g = (tid - W2_S0) >> 5;
     if (g < ngrp) {
       const int slot = 32 * g + (tid & 31);
       const bool act = slot < 4 * P.nk;
@@ -1165,7 +1169,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   } else {
     // ------------------------------------------------------------ FH role
     asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
-    const int o = tid - W2_V - W2_S;
+    const int o = tid - W2_H0;
     const bool act = o < TWv;
     if ((o & ~31) >= TWv) {   // warp wholly past the strip: only the barriers
       for (int y = y0; y < yend; ++y) {
