@@ -216,6 +216,28 @@ def test_kernels_agree_bitwise(gpu, cfg, H, W, monkeypatch):
     assert_parity(outs["ws2"], bf.bf_box(img, op), spec.intensity_max, cfg)
 
 
+@pytest.mark.parametrize("cfg,H,W,over", [("cfg1", 140, 300, {"range_kind": "tukey", "sigma_r": 40.0, "n_terms": 12}),
+                                          ("cfg0", 120, 250, {"range_kind": "tukey", "sigma_r": 40.0, "n_terms": 13}),
+                                          ("cfg2", 150, 330, {"n_terms": 5})])
+def test_kernels_agree_nonconsecutive_and_partial(gpu, cfg, H, W, over, monkeypatch):
+    """Tukey plans select non-consecutive k (the CONSEC = false instantiations, a runtime
+    recurrence step count per term) and N_eff < MAXK leaves a partial channel group (FULL =
+    false): the three kernels agree bitwise there too, and match the oracle."""
+    pkg, torch = gpu
+    spec = CONFIGS[cfg]
+    img = config_input(spec, H=H, W=W)
+    gp, op = make_plans(pkg, config_params(spec), img.dtype, **over)
+    if over.get("range_kind") == "tukey":
+        ks = gp.info()["k"]
+        assert any(b - a > 1 for a, b in zip(ks, ks[1:])), ks
+    outs = {}
+    for k in ("band", "ws", "ws2"):
+        monkeypatch.setenv("BF_KERNEL", k)
+        outs[k] = run_gpu(pkg, torch, gp, img)
+    assert np.array_equal(outs["band"], outs["ws"]) and np.array_equal(outs["band"], outs["ws2"])
+    assert_parity(outs["ws2"], bf.bf_box(img, op), spec.intensity_max, cfg)
+
+
 def test_multi_plan_case1_shared_channels(gpu):
     """bf_apply_multi (Case 1 of P:1200-1219): several range kernels over one pass of shared
     box-filtered channels. Each plan's image matches the oracle of that plan (and the plan's own
