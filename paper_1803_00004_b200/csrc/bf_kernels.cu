@@ -385,7 +385,8 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           Ucol[(t * 4 * nk + 4 * i + c) * UP] = U[t * 4 * MAXK + 4 * i + c] >> P.ush;
-      if (hook && ((i & 7) == 7 || i + 1 == nk)) hook->end(i >> 3);   // channel group i / 8 written
+      // channel group i / 8 written (FULL: the last term is known at compile time)
+      if (hook && ((i & 7) == 7 || (FULL ? i + 1 == MAXK : i + 1 == nk))) hook->end(i >> 3);
     }
   }
 }
@@ -1228,7 +1229,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
           den = mad_wide(wsn, F[1], den);
           num = mad_wide(wc, F[2], num);
           num = mad_wide(wsn, F[3], num);
-          if ((i & 7) == 7 || i + 1 == P.nk) bar_arrive(BAR_U_EMPTY + 2 * b + (i >> 3), n_uempty);
+          if ((i & 7) == 7 || (FULL ? i + 1 == MAXK : i + 1 == P.nk)) bar_arrive(BAR_U_EMPTY + 2 * b + (i >> 3), n_uempty);
         }
       }
       if (act) finish_pixel(P, num, den, Ic, prow + (long long)y * P.W, out, ws);
