@@ -174,8 +174,12 @@ BF_API bf_status bf_apply_multi(const bf_plan* const* plans, int n_plans, const 
                                 bf_stream stream);
 
 /* Host-to-host convenience for end-to-end timing: copies h_in (host) to the device, filters,
- * copies the result back into h_out (host) and synchronises `stream`. Device buffers come
- * from a library-owned cache keyed by size (grown on demand, freed at exit). */
+ * copies the result back into h_out (host) and synchronises `stream`. Large images run as up to
+ * five row chunks pipelined over library-owned streams (ordered after the work already in
+ * `stream`): the copy of the next input piece, the filter of the current chunk and the copy back
+ * of the previous chunk overlap. Pinned host buffers make the copies asynchronous. Device
+ * buffers come from a library-owned cache keyed by size (grown on demand, freed at exit; one
+ * device per process). Results equal bf_apply's bitwise. */
 BF_API bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float* h_out, int H, int W, bf_stream stream);
 
 /*

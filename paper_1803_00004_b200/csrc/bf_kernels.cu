@@ -51,6 +51,7 @@ struct KParams {
   int H, W;
   long long frame_elems;
   int TW, TH, rlo_x;
+  int yb, ye;                 // output rows [yb, ye) of this launch (bf_apply_host pipelines row chunks)
   int ns;                     // box-pair terms: K~_s = sum_{s < ns} fx_s(u) fy_s(v) (1 = separable)
   int nby;                    // vertical boxes (shared by the ns terms: one set of taps)
   int vlo[MAXB], vhi[MAXB];   // vertical boxes: row offsets (inclusive)
@@ -805,12 +806,12 @@ __global__ void __launch_bounds__(NT, (Occ<MAXK, NT>::value))
 
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * P.TW;
-  const int y0 = blockIdx.y * P.TH;
+  const int y0 = P.yb + blockIdx.y * P.TH;
   const long long fbase = (long long)blockIdx.z * P.frame_elems;
   const int col = x0 - P.rlo_x + tid;
   const bool colok = (col >= 0) & (col < P.W);
   const int TWv = min(P.TW, P.W - x0);
-  const int yend = min(y0 + P.TH, P.H);
+  const int yend = min(y0 + P.TH, P.ye);
 
   fill_luts<U8>(P, lut, lut64, tid, NT);
   if (U8) __syncthreads();
@@ -908,10 +909,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * P.TW;
-  const int y0 = blockIdx.y * P.TH;
+  const int y0 = P.yb + blockIdx.y * P.TH;
   const long long fbase = (long long)blockIdx.z * P.frame_elems;
   const int TWv = min(P.TW, P.W - x0);
-  const int yend = min(y0 + P.TH, P.H);
+  const int yend = min(y0 + P.TH, P.ye);
   const int ngrp = P.ngrp;                       // channel groups (1 or 2)
   const int nfw = (WS_F / 32) / ngrp;            // F warps per group
   const int n_uempty = WS_V + 32 * nfw;          // U_EMPTY: F_g arrive, V sync
@@ -1104,10 +1105,10 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
 
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * P.TW;
-  const int y0 = blockIdx.y * P.TH;
+  const int y0 = P.yb + blockIdx.y * P.TH;
   const long long fbase = (long long)blockIdx.z * P.frame_elems;
   const int TWv = min(P.TW, P.W - x0);
-  const int yend = min(y0 + P.TH, P.H);
+  const int yend = min(y0 + P.TH, P.ye);
   const int wv = P.wv;                            // extended columns scanned (multiple of 8, <= W2_V)
   const int ngrp = P.ngrp;                        // channel groups (1 or 2)
   constexpr int n_ufull = W2_V + 32;              // U_FULL: V arrive, S_g sync
@@ -1660,8 +1661,12 @@ bool same_channels(const bf_plan* a, const bf_plan* b) {
 }
 
 // dry != nullptr: describe the launches (bf_apply_config) instead of enqueueing them
+// ya, yb: output rows [ya, yb) (default: all); the input rows the halo needs must be resident.
 bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, float* d_out, int n_frames, int H,
-                     int W, cudaStream_t st, bf_launch_config* dry = nullptr) {
+                     int W, cudaStream_t st, bf_launch_config* dry = nullptr, int ya = 0, int yb = -1) {
+  if (yb < 0) yb = H;
+  if (ya < 0 || ya >= yb || yb > H) return BF_ERR_INVALID_ARG;
+  const int Hr = yb - ya;
   if (!plans || nplans < 1 || nplans > MAXP || (!dry && (!d_in || !d_out)) || H <= 0 || W <= 0 || n_frames <= 0)
     return BF_ERR_INVALID_ARG;
   for (int q = 0; q < nplans; ++q)
@@ -1686,7 +1691,7 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
   }
   const bf_plan* p = &merged;
   if (p->literal) {
-    if (nplans != 1) return BF_ERR_UNSUPPORTED;
+    if (nplans != 1 || ya != 0 || yb != H) return BF_ERR_UNSUPPORTED;
     return run_literal(p, d_in, d_out, n_frames, H, W, st, dry);
   }
   if ((long long)H * W > (1LL << 40) / n_frames) return BF_ERR_INVALID_ARG;
@@ -1720,6 +1725,8 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
   std::memset(&P, 0, sizeof(P));
   P.H = H;
   P.W = W;
+  P.yb = ya;
+  P.ye = yb;
   P.frame_elems = (long long)H * W;
   P.TW = TW;
   P.rlo_x = rlo;
@@ -1829,8 +1836,8 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
       init = std::max(1500.0, 373.0 * ((wv + 31) / 32) / (4 * 0.55));
     }
     const long long strips = (W + tw - 1) / tw;
-    for (int nb = 1; nb <= H; ++nb) {
-      const int TH = (H + nb - 1) / nb;
+    for (int nb = 1; nb <= Hr; ++nb) {
+      const int TH = (Hr + nb - 1) / nb;
       if (nb > 1 && TH < 16) break;
       const long long ctas = strips * nb * n_frames;
       const long long waves = (ctas + slots - 1) / slots;
@@ -1845,9 +1852,9 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
   TW = best_tw;
   P.TW = TW;
   const int nstrips = (W + TW - 1) / TW;
-  P.TH = (H + best_nb - 1) / best_nb;
-  if (const char* e = std::getenv("BF_TH")) P.TH = std::max(1, std::min(H, std::atoi(e)));   // test hook
-  best_nb = (H + P.TH - 1) / P.TH;
+  P.TH = (Hr + best_nb - 1) / best_nb;
+  if (const char* e = std::getenv("BF_TH")) P.TH = std::max(1, std::min(Hr, std::atoi(e)));   // test hook
+  best_nb = (Hr + P.TH - 1) / P.TH;
 
   if (dry) {
     KParams Q = P;
@@ -1923,16 +1930,36 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
   return err == cudaSuccess ? BF_OK : BF_ERR_CUDA;
 }
 
-// Device buffers for bf_apply_host, grown on demand.
+// Device buffers, streams and events for bf_apply_host (grown / created on demand, per process
+// and device).
+constexpr int HOST_CHUNKS = 5;
 struct HostCache {
   std::mutex mu;
+  int dev = -1;
   void* din = nullptr;
   float* dout = nullptr;
   size_t in_bytes = 0, out_bytes = 0;
+  cudaStream_t s_in = nullptr, s_k = nullptr, s_out = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_in[HOST_CHUNKS] = {}, ev_k[HOST_CHUNKS] = {};
   ~HostCache() {
     // freed at process exit; the CUDA context may already be gone, so errors are ignored
     if (din) cudaFree(din);
     if (dout) cudaFree(dout);
+  }
+  cudaError_t setup(int device) {
+    if (dev == device) return cudaSuccess;
+    if (dev >= 0) return cudaErrorInvalidDevice;   // one device per process (torchrun ranks)
+    cudaError_t e = cudaSuccess;
+    for (cudaStream_t* q : {&s_in, &s_k, &s_out})
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(q, cudaStreamNonBlocking);
+    for (cudaEvent_t* v : {&ev_start, &ev_end})
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(v, cudaEventDisableTiming);
+    for (int j = 0; j < HOST_CHUNKS && e == cudaSuccess; ++j) {
+      e = cudaEventCreateWithFlags(&ev_in[j], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_k[j], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) dev = device;
+    return e;
   }
 };
 HostCache g_cache;
@@ -1977,8 +2004,11 @@ extern "C" bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float*
   if (!plan || !h_in || !h_out || H <= 0 || W <= 0) return BF_ERR_INVALID_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t n = (size_t)H * W;
-  const size_t ib = n * (plan->input_dtype == BF_IN_U8 ? 1 : 4), ob = n * 4;
+  const size_t isz = plan->input_dtype == BF_IN_U8 ? 1 : 4;
+  const size_t ib = n * isz, ob = n * 4;
   std::lock_guard<std::mutex> lk(g_cache.mu);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || g_cache.setup(dev) != cudaSuccess) return BF_ERR_CUDA;
   if (g_cache.in_bytes < ib) {
     if (g_cache.din) cudaFree(g_cache.din);
     g_cache.din = nullptr;
@@ -1991,10 +2021,54 @@ extern "C" bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float*
     if (cudaMalloc(&g_cache.dout, ob) != cudaSuccess) return BF_ERR_CUDA;
     g_cache.out_bytes = ob;
   }
-  if (cudaMemcpyAsync(g_cache.din, h_in, ib, cudaMemcpyHostToDevice, st) != cudaSuccess) return BF_ERR_CUDA;
-  bf_status s = run_filter(&plan, 1, g_cache.din, g_cache.dout, 1, H, W, st);
+  // Row chunks pipelined over three streams: the copy of input piece j+1, the filter of output
+  // rows [b_j, b_j+1) and the copy back of chunk j-1 overlap. Input piece j holds rows
+  // [b_j + rv, b_j+1 + rv) (piece 0 from row 0, the last to row H), so the filter of chunk j,
+  // which reads rows b_j - rv .. b_j+1 - 1 + rv, needs pieces 0..j only. Small images, the
+  // literal kernel and chunks shorter than 512 rows take one chunk.
+  int rv = 0;
+  for (int b = 0; b < plan->snby[0]; ++b) rv = std::max(rv, std::max(-plan->sloy[0][b], plan->shiy[0][b]));
+  // K chunks, the first and the last half as tall as the others (the pipeline's fill and drain
+  // are one input piece and one output chunk)
+  int K = plan->literal || n < (1u << 20) ? 1 : std::min(HOST_CHUNKS, 1 + H / std::max(512, 2 * rv + 2));
+  K = std::max(K, 1);
+  cudaError_t e = cudaEventRecord(g_cache.ev_start, st);   // ordered after the caller's prior work
+  for (cudaStream_t q : {g_cache.s_in, g_cache.s_k, g_cache.s_out})
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(q, g_cache.ev_start, 0);
+  if (e != cudaSuccess) return BF_ERR_CUDA;
+  const unsigned char* hin = static_cast<const unsigned char*>(h_in);
+  unsigned char* din = static_cast<unsigned char*>(g_cache.din);
+  auto bnd = [&](int j) {   // boundary j of K chunks with weights 1/2, 1, ..., 1, 1/2
+    if (K <= 2) return (int)((long long)H * j / K);
+    if (j <= 0) return 0;
+    if (j >= K) return H;
+    return (int)((long long)H * (2 * j - 1) / (2 * (K - 1)));
+  };
+  for (int j = 0; j < K && e == cudaSuccess; ++j) {
+    const int r0 = j == 0 ? 0 : std::min(H, bnd(j) + rv), r1 = j == K - 1 ? H : std::min(H, bnd(j + 1) + rv);
+    if (r1 > r0)
+      e = cudaMemcpyAsync(din + (size_t)r0 * W * isz, hin + (size_t)r0 * W * isz, (size_t)(r1 - r0) * W * isz,
+                          cudaMemcpyHostToDevice, g_cache.s_in);
+    if (e == cudaSuccess) e = cudaEventRecord(g_cache.ev_in[j], g_cache.s_in);
+  }
+  bf_status s = BF_OK;
+  for (int j = 0; j < K && e == cudaSuccess && s == BF_OK; ++j) {
+    e = cudaStreamWaitEvent(g_cache.s_k, g_cache.ev_in[j], 0);
+    if (e != cudaSuccess) break;
+    s = run_filter(&plan, 1, g_cache.din, g_cache.dout, 1, H, W, g_cache.s_k, nullptr, bnd(j), bnd(j + 1));
+    if (s != BF_OK) break;
+    e = cudaEventRecord(g_cache.ev_k[j], g_cache.s_k);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(g_cache.s_out, g_cache.ev_k[j], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h_out + (size_t)bnd(j) * W, g_cache.dout + (size_t)bnd(j) * W,
+                          (size_t)(bnd(j + 1) - bnd(j)) * W * 4, cudaMemcpyDeviceToHost, g_cache.s_out);
+  }
+  // join: the caller's stream waits for all three, then the call returns with h_out complete
+  for (cudaStream_t q : {g_cache.s_in, g_cache.s_k, g_cache.s_out}) {
+    cudaEventRecord(g_cache.ev_end, q);
+    cudaStreamWaitEvent(st, g_cache.ev_end, 0);
+  }
+  const cudaError_t es = cudaStreamSynchronize(st);
   if (s != BF_OK) return s;
-  if (cudaMemcpyAsync(h_out, g_cache.dout, ob, cudaMemcpyDeviceToHost, st) != cudaSuccess) return BF_ERR_CUDA;
-  if (cudaStreamSynchronize(st) != cudaSuccess) return BF_ERR_CUDA;
-  return BF_OK;
+  return (e == cudaSuccess && es == cudaSuccess) ? BF_OK : BF_ERR_CUDA;
 }

@@ -116,6 +116,23 @@ def test_cfg3_batched_frames_match_single_calls(gpu):
         assert_parity(single, bf.bf_box(frames[f], op), 255.0, f"frame {f}")
 
 
+@pytest.mark.parametrize("cfg,H,W", [("cfg2", 2048, 600), ("cfg4", 2100, 520), ("cfg0", 1100, 1000), ("cfg1", 90, 77)])
+def test_host_path_matches_device_path(gpu, cfg, H, W):
+    """bf_apply_host pipelines row chunks (input piece j+1 copied while chunk j is filtered and
+    chunk j-1 copied back; each chunk a separate row-range launch with its own band tiling). The
+    integer pipeline makes every output independent of the tiling, so the host path must equal
+    the one-launch device path bitwise (cfg4: three passes through the workspace per chunk)."""
+    pkg, torch = gpu
+    spec = CONFIGS[cfg]
+    img = config_input(spec, H=H, W=W)
+    gp, _ = make_plans(pkg, config_params(spec), img.dtype)
+    dev = run_gpu(pkg, torch, gp, img)
+    h_in = torch.from_numpy(img).pin_memory()
+    h_out = torch.full((H, W), float("nan"), dtype=torch.float32).pin_memory()
+    pkg.apply_host(gp, h_in.data_ptr(), h_out.data_ptr(), H, W, torch.cuda.current_stream().cuda_stream)
+    assert np.array_equal(h_out.numpy().astype(np.float64), dev)
+
+
 # ------------------------------------------------------------------ edge cases
 
 @pytest.mark.parametrize("H,W", [(1, 1), (1, 57), (61, 1), (5, 7), (7, 300), (300, 6), (17, 33)])
