@@ -1932,14 +1932,14 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
 
 // Device buffers, streams and events for bf_apply_host (grown / created on demand, per process
 // and device).
-constexpr int HOST_CHUNKS = 5;
+constexpr int HOST_CHUNKS = 9, HOST_CHUNKS_DEFAULT = 5;
 struct HostCache {
   std::mutex mu;
   int dev = -1;
   void* din = nullptr;
   float* dout = nullptr;
   size_t in_bytes = 0, out_bytes = 0;
-  cudaStream_t s_in = nullptr, s_k = nullptr, s_out = nullptr;
+  cudaStream_t s_in = nullptr, s_k = nullptr, s_k2 = nullptr, s_out = nullptr;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_in[HOST_CHUNKS] = {}, ev_k[HOST_CHUNKS] = {};
   ~HostCache() {
     // freed at process exit; the CUDA context may already be gone, so errors are ignored
@@ -1950,7 +1950,7 @@ struct HostCache {
     if (dev == device) return cudaSuccess;
     if (dev >= 0) return cudaErrorInvalidDevice;   // one device per process (torchrun ranks)
     cudaError_t e = cudaSuccess;
-    for (cudaStream_t* q : {&s_in, &s_k, &s_out})
+    for (cudaStream_t* q : {&s_in, &s_k, &s_k2, &s_out})
       if (e == cudaSuccess) e = cudaStreamCreateWithFlags(q, cudaStreamNonBlocking);
     for (cudaEvent_t* v : {&ev_start, &ev_end})
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(v, cudaEventDisableTiming);
@@ -2030,10 +2030,12 @@ extern "C" bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float*
   for (int b = 0; b < plan->snby[0]; ++b) rv = std::max(rv, std::max(-plan->sloy[0][b], plan->shiy[0][b]));
   // K chunks, the first and the last half as tall as the others (the pipeline's fill and drain
   // are one input piece and one output chunk)
-  int K = plan->literal || n < (1u << 20) ? 1 : std::min(HOST_CHUNKS, 1 + H / std::max(512, 2 * rv + 2));
+  int K = plan->literal || n < (1u << 20) ? 1 : std::min(HOST_CHUNKS_DEFAULT, 1 + H / std::max(512, 2 * rv + 2));
+  if (const char* ev = std::getenv("BF_HOST_CHUNKS"))   // tuning hook
+    K = std::min(HOST_CHUNKS, std::max(1, std::min(std::atoi(ev), H / std::max(1, 2 * rv + 2))));
   K = std::max(K, 1);
   cudaError_t e = cudaEventRecord(g_cache.ev_start, st);   // ordered after the caller's prior work
-  for (cudaStream_t q : {g_cache.s_in, g_cache.s_k, g_cache.s_out})
+  for (cudaStream_t q : {g_cache.s_in, g_cache.s_k, g_cache.s_k2, g_cache.s_out})
     if (e == cudaSuccess) e = cudaStreamWaitEvent(q, g_cache.ev_start, 0);
   if (e != cudaSuccess) return BF_ERR_CUDA;
   const unsigned char* hin = static_cast<const unsigned char*>(h_in);
@@ -2053,18 +2055,20 @@ extern "C" bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float*
   }
   bf_status s = BF_OK;
   for (int j = 0; j < K && e == cudaSuccess && s == BF_OK; ++j) {
-    e = cudaStreamWaitEvent(g_cache.s_k, g_cache.ev_in[j], 0);
+    // alternate two compute streams: chunk j+1 may start on the SMs chunk j's last CTAs leave
+    cudaStream_t sk = (j & 1) ? g_cache.s_k2 : g_cache.s_k;
+    e = cudaStreamWaitEvent(sk, g_cache.ev_in[j], 0);
     if (e != cudaSuccess) break;
-    s = run_filter(&plan, 1, g_cache.din, g_cache.dout, 1, H, W, g_cache.s_k, nullptr, bnd(j), bnd(j + 1));
+    s = run_filter(&plan, 1, g_cache.din, g_cache.dout, 1, H, W, sk, nullptr, bnd(j), bnd(j + 1));
     if (s != BF_OK) break;
-    e = cudaEventRecord(g_cache.ev_k[j], g_cache.s_k);
+    e = cudaEventRecord(g_cache.ev_k[j], sk);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(g_cache.s_out, g_cache.ev_k[j], 0);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(h_out + (size_t)bnd(j) * W, g_cache.dout + (size_t)bnd(j) * W,
                           (size_t)(bnd(j + 1) - bnd(j)) * W * 4, cudaMemcpyDeviceToHost, g_cache.s_out);
   }
   // join: the caller's stream waits for all three, then the call returns with h_out complete
-  for (cudaStream_t q : {g_cache.s_in, g_cache.s_k, g_cache.s_out}) {
+  for (cudaStream_t q : {g_cache.s_in, g_cache.s_k, g_cache.s_k2, g_cache.s_out}) {
     cudaEventRecord(g_cache.ev_end, q);
     cudaStreamWaitEvent(st, g_cache.ev_end, 0);
   }
