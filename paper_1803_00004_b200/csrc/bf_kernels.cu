@@ -1055,7 +1055,7 @@ constexpr int W2_UP = W2_V + 4;   // == 4 mod 32: conflict-free LDS.128 / STS.12
 // IADD3 per column); int32 wrap-around keeps every box difference exact. Q[n] = total.
 __device__ __forceinline__ void prefix_row(int* Q, int n) {
   int carry = 0;
-#pragma unroll 2
+#pragma unroll 8
   for (int e = 0; e < n; e += 8) {
     const int4 a = *reinterpret_cast<const int4*>(Q + e), b = *reinterpret_cast<const int4*>(Q + e + 4);
     const int o1 = carry + a.x;
