@@ -1,28 +1,28 @@
-// Fused sm_100a kernel of the joint-acceleration bilateral filter (bf_apply), version 6.
+// sm_100a kernels of the joint-acceleration bilateral filter (bf_apply) and their host dispatch.
 //
 // Evaluates eq:numerator_2D_box_N_terms with T = D (Q1): for every selected cosine
 // term k the four channels g^c_k = cos(w_k I), g^s_k = sin(w_k I), G^c_k = I g^c_k,
-// G^s_k = I g^s_k are generated in registers, box-filtered with the separable Haar-box
-// kernel K~_s(u, v) = fx(u) fy(v) (eq:2D_box_N_terms_s, Appendix A), and recombined
-// with a_k g^c_k(x), a_k g^s_k(x) (Q17); out = num / den (eq:BF).
+// G^s_k = I g^s_k are generated in registers, box-filtered with the Haar-box kernel
+// K~_s (eq:2D_box_N_terms_s, Appendix A; separable, or rank 2 for N_s = 5), and
+// recombined with a_k g^c_k(x), a_k g^s_k(x) (Q17); out = num / den (eq:BF).
 //
-// A CTA owns a vertical strip (NT extended columns = TW output columns plus the horizontal
-// halo, one thread per extended column) and a band of TH output rows. Per output row y it runs
-// two barrier-separated intervals:
-//   A  V(y): every thread slides the vertical box sums of all channels of its column down one
-//      row. The box weight wy_b is folded into the per-tap quantisation scale, so the state is
-//      ONE exact int32 per channel (U = sum_b sum_v rint(wy_b X 2^q)); taps are regenerated
-//      from I by a Chebyshev recurrence (cos (k+1)t = 2 cos t cos kt - cos (k-1)t) from a
-//      polynomial (f32) or LUT (u8) base angle and quantised with one FFMA2 per tap pair
-//      (x*s + 1.5*2^23 has the integer rint(x*s) in its low mantissa bits). U' = U >> ush goes
-//      to shared memory.
-//      C(y-1): one thread per output pixel computes the combine weights a_k cos/sin(k pi I(x)/D)
-//      in fp64 (Chebyshev again), rounds them to integers with the fp64 magic-number trick,
-//      accumulates num / den exactly in int64 from the F row of y-1 and writes D*num/den (or
-//      I(x) if den <= 0, Q18).
-//   B  H(y): walkers slide the exact int32 horizontal box sums of U' along the row. Lanes of a
-//      warp are 32 channels at the SAME x (conflict-free shared-memory access); each writes
-//      F = sum_b ax_b H_b (exact int64, narrowed to int32) to shared memory.
+// A CTA owns a vertical strip (TW output columns plus the horizontal halo) and a band of TH
+// output rows. Per row y, in every kernel:
+//   V(y)  one thread per extended column slides the vertical box sums of all channels down one
+//         row. The box weight wy_b is folded into the per-tap quantisation scale, so the state
+//         is ONE exact int32 per channel (U = sum_b sum_v rint(wy_b X 2^q)); the taps' channels
+//         come from a polynomial (f32) or LUT (u8) base angle and the rotation recurrence, and
+//         are quantised with one FFMA2 per tap pair (x*s + 1.5*2^23 holds rint(x*s) in its low
+//         mantissa bits). U' = U >> ush goes to shared memory.
+//   H(y)  exact int32 horizontal box sums H_b of U', weighted into F = sum_b mulhi(H_b, ax_b):
+//         by walkers (kernel 1) or as differences of in-place prefix rows (kernels 2, 2b).
+//   C(y)  per output pixel: combine weights a_k cos/sin(k pi I(x)/D) in fp64, rounded to int32,
+//         num / den accumulated exactly in int64; out = D num / den (or I(x) if den <= 0, Q18).
+// Kernel 1 (bf_band_kernel) runs V / C and H in barrier-separated intervals; kernel 2
+// (bf_ws_kernel) and kernel 2b (bf_ws2_kernel, the default) specialise warps by role and hand
+// rows over through named barriers, kernel 2b fusing the box differences into the combine.
+// Kernel 3 (bf_literal_kernel) is the paper-literal z-window on u8 levels (NEXT f1). All three
+// T = D kernels perform the same integer arithmetic: their outputs are bitwise equal.
 // Nothing but the input image and the output image touches HBM (plus an int64 num/den
 // workspace when the terms do not fit one pass).
 #include <cuda_runtime.h>
@@ -1441,8 +1441,8 @@ cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim
       }
       return cudaErrorInvalidConfiguration;
     }
-    if (kern == KERN_WS) {
-      auto kfn = bf_ws_kernel<MAXK, FORM, U8, CONSEC, FULL, MULTI>;
+    if (kern == KERN_WS && !MULTI) {   // (the Case 1 multi-plan combine runs on kernel 1)
+      auto kfn = bf_ws_kernel<MAXK, FORM, U8, CONSEC, FULL, false>;
       const size_t smem = smem_layout_ws(P, MAXK, U8);
       if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
       cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
