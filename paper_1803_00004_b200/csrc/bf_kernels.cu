@@ -296,7 +296,7 @@ __device__ __forceinline__ void v_init(const KParams& P, const void* __restrict_
         if (i > 0) {
           if (CONSEC) rot1(gc, gs, c1, s1);
           else
-            for (int j = 0; j < P.kstep[i]; ++j) rot1(gc, gs, c1, s1);
+            for (int j = 0; j < P.kstep[i]; ++j) rot1(gc, gs, c1, s1);   // (init rows only)
         }
 #pragma unroll
         for (int t = 0; t < NS; ++t)
@@ -364,13 +364,16 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
   for (int i = 0; i < MAXK; ++i) {
     if (FULL || i < nk) {
       if (hook && (i & 7) == 0) hook->begin(i >> 3);   // channel group i / 8 starts: its buffer free
+      if (i > 0) {   // k_i - k_{i-1} >= 1 recurrence steps, all boxes under one loop test
+#pragma unroll
+        for (int b = 0; b < NB; ++b) g2[b].step();
+        if (!CONSEC)
+          for (int j = 1; j < P.kstep[i]; ++j)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) g2[b].step();
+      }
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
-        if (i > 0) {
-          if (CONSEC) g2[b].step();
-          else
-            for (int j = 0; j < P.kstep[i]; ++j) g2[b].step();
-        }
         const u64 C = g2[b].C, Sn = g2[b].S;
 #pragma unroll
         for (int t = 0; t < NS; ++t) {
@@ -1212,10 +1215,10 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       for (int i = 0; i < MAXK; ++i) {
         if (FULL || i < P.nk) {
           if ((i & 7) == 0) bar_sync(BAR_Q_FULL + 2 * b + (i >> 3), n_qfull);
-          if (i > 0) {
-            if (CONSEC) gk.step();
-            else
-              for (int j = 0; j < P.kstep[i]; ++j) gk.step();
+          if (i > 0) {   // k_i - k_{i-1} >= 1 steps
+            gk.step();
+            if (!CONSEC)
+              for (int j = 1; j < P.kstep[i]; ++j) gk.step();
           }
           const int wc = __double2loint(fma(gk.c, P.aw[0][i], MAGIC64));
           const int wsn = __double2loint(fma(gk.s, P.aw[0][i], MAGIC64));
