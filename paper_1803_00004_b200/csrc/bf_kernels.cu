@@ -1914,6 +1914,10 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
     int nseg = std::max(1, max_tasks / P.ngrp);
     const int min_len = sh.kern == KERN_WS ? 24 : std::max(32, 2 * (rlo + rhi + 1) / 3);
     while (nseg > 1 && (TW + nseg - 1) / nseg < min_len) --nseg;
+    // wide halos (NT = 512): the other warps idle through interval B behind one long walker;
+    // four segments measured best on cfg4 (r = 192: 77.0 -> 62.2 ms; 1 / 2 / 8 / 16 segments:
+    // 77.0 / 67.0 / 67.7 / 82.5 ms)
+    if (sh.kern == KERN_BAND && sh.NT == 512) nseg = std::min(4, std::max(1, max_tasks / P.ngrp));
     if (const char* e = std::getenv("BF_NSEG")) nseg = std::max(1, std::min(max_tasks / P.ngrp, std::atoi(e)));  // tuning hook
     P.nseg = nseg;
     P.seglen = (TW + nseg - 1) / nseg;
