@@ -2047,11 +2047,14 @@ extern "C" bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float*
   if (e != cudaSuccess) return BF_ERR_CUDA;
   const unsigned char* hin = static_cast<const unsigned char*>(h_in);
   unsigned char* din = static_cast<unsigned char*>(g_cache.din);
-  auto bnd = [&](int j) {   // boundary j of K chunks with weights 1/2, 1, ..., 1, 1/2
+  // boundary j of K chunks with weights w, 1, ..., 1, w (w = 1/2; BF_HOST_EDGE = 1/w tuning hook)
+  int edge = 2;
+  if (const char* ev = std::getenv("BF_HOST_EDGE")) edge = std::max(1, std::atoi(ev));
+  auto bnd = [&](int j) {
     if (K <= 2) return (int)((long long)H * j / K);
     if (j <= 0) return 0;
     if (j >= K) return H;
-    return (int)((long long)H * (2 * j - 1) / (2 * (K - 1)));
+    return (int)((long long)H * (edge * (j - 1) + 1) / (edge * (K - 2) + 2));
   };
   for (int j = 0; j < K && e == cudaSuccess; ++j) {
     const int r0 = j == 0 ? 0 : std::min(H, bnd(j) + rv), r1 = j == K - 1 ? H : std::min(H, bnd(j + 1) + rv);
