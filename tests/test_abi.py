@@ -122,11 +122,11 @@ def test_plan_edge_parameters(bfmod):
 
 
 def test_launch_count_query(bfmod):
-    """bf_apply_launches: one launch when the terms fit one pass, ceil(N / 8) at r = 192 (cfg4),
-    argument validation; host-only (no device work)."""
+    """bf_apply_launches: one launch when the terms fit one pass, ceil(N / 16) at r = 192 (cfg4:
+    24 terms), argument validation; host-only (no device work)."""
     import ctypes as C
     L = bfmod.lib()
-    for cfg, want in (("cfg0", 1), ("cfg2", 1), ("cfg3", 1), ("cfg4", 3)):
+    for cfg, want in (("cfg0", 1), ("cfg2", 1), ("cfg3", 1), ("cfg4", 2)):
         p = config_params(CONFIGS[cfg])
         plan = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"],
                           sigma_r=p["sigma_r"], radius=p["radius"], n_terms=p["n_terms"],
@@ -141,11 +141,11 @@ def test_launch_config_query(bfmod, monkeypatch):
     """bf_apply_config describes the launches without device work: the fused warp-specialised
     kernel (768 threads, at most 384 - halo output columns per strip, narrower strips where they
     fill the SMs better) for the separable N_s = 9 plans, the
-    band kernel for cfg4's r = 192 halo (3 passes), the literal kernel for range_window='literal';
+    band kernel for cfg4's r = 192 halo (2 passes), the literal kernel for range_window='literal';
     BF_KERNEL forces a kernel; the grid covers the image."""
     import ctypes as C
     for cfg, kern, launches in (("cfg2", "bf_ws2_kernel", 1), ("cfg1", "bf_ws2_kernel", 1),
-                                ("cfg4", "bf_band_kernel", 3)):
+                                ("cfg4", "bf_band_kernel", 2)):
         spec = CONFIGS[cfg]
         p = config_params(spec)
         plan = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"],

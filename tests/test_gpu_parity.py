@@ -58,7 +58,7 @@ SMALL = {
     "cfg1": (300, 347),
     "cfg2": (333, 361),          # r = 48: 3 strips (TW = 160) + ragged tail, 2 bands
     "cfg3": (211, 333),
-    "cfg4": (419, 430),          # r = 192, Tukey, 24 terms: 3 passes, 4 strips
+    "cfg4": (419, 430),          # r = 192, Tukey, 24 terms: 2 passes, 4 strips
 }
 
 
@@ -121,7 +121,7 @@ def test_host_path_matches_device_path(gpu, cfg, H, W):
     """bf_apply_host pipelines row chunks (input piece j+1 copied while chunk j is filtered and
     chunk j-1 copied back; each chunk a separate row-range launch with its own band tiling). The
     integer pipeline makes every output independent of the tiling, so the host path must equal
-    the one-launch device path bitwise (cfg4: three passes through the workspace per chunk)."""
+    the one-launch device path bitwise (cfg4: two passes through the workspace per chunk)."""
     pkg, torch = gpu
     spec = CONFIGS[cfg]
     img = config_input(spec, H=H, W=W)
