@@ -1044,7 +1044,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 //   warps 0-9    FH: one thread per output pixel: for every channel slot of group g,
 //                F = sum_b mulhi(Q[x + hi_b + 1] - Q[x + lo_b], ax_b) (lanes = consecutive
 //                x: conflict-free), accumulated straight into the exact int64 num / den with the
-//                pixel's fp64 combine weights; then out = D num / den
+//                pixel's fp64 combine weights (per range plan for bf_apply_multi); then out = D num / den
 // setmaxnreg: V 112, S / FH 48 (768 x 80 at launch). Named barriers:
 //   U_FULL(b,g) 0-3   V arrive, S_g sync        U_EMPTY(b,g) 4-7  FH arrive, V sync
 //   Q_FULL(b,g) 8-11  S_g arrive, FH sync       (b = row parity, g = channel group)
@@ -1092,11 +1092,12 @@ __device__ __forceinline__ void finish_pixel(const KParams& P, long long num, lo
   else out[pix] = (den > 0) ? (float)(P.D * (double)num / (double)den) : Ic;
 }
 
-template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL>
+template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL, bool MULTI>
 __global__ void __launch_bounds__(W2_THREADS, 1)
     bf_ws2_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out, longlong2* __restrict__ ws) {
   constexpr int NS = Form<FORM>::NS, NB = Form<FORM>::NBY, NBX = Form<FORM>::NBX;
   constexpr int M = NS * NBX;
+  constexpr int NPL = MULTI ? MAXP : 1;   // range plans combined per pixel
   static_assert(NS == 1 && M <= 2, "the FH role handles separable forms with at most two x boxes");
   constexpr int UP = W2_UP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1210,7 +1211,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       gk.init(c1, s1);
       for (int j = 0; j < P.kstep[0]; ++j) gk.step();
       const int* Qb = Ubuf + b * ustride;
-      long long num = 0, den = 0;
+      long long num[NPL] = {}, den[NPL] = {};
 #pragma unroll
       for (int i = 0; i < MAXK; ++i) {
         if (FULL || i < P.nk) {
@@ -1220,8 +1221,6 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
             if (!CONSEC)
               for (int j = 1; j < P.kstep[i]; ++j) gk.step();
           }
-          const int wc = __double2loint(fma(gk.c, P.aw[0][i], MAGIC64));
-          const int wsn = __double2loint(fma(gk.s, P.aw[0][i], MAGIC64));
           int F[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -1229,14 +1228,25 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
             F[c] = __mulhi(q[e0] - q[l0], ax0);
             if (M == 2) F[c] += __mulhi(q[e1] - q[l1], ax1);
           }
-          den = mad_wide(wc, F[0], den);
-          den = mad_wide(wsn, F[1], den);
-          num = mad_wide(wc, F[2], num);
-          num = mad_wide(wsn, F[3], num);
+#pragma unroll
+          for (int q = 0; q < NPL; ++q) {   // Case 1 (bf_apply_multi): every plan over the same F
+            if (q == 0 || q < P.nplans) {
+              const int wc = __double2loint(fma(gk.c, P.aw[q][i], MAGIC64));
+              const int wsn = __double2loint(fma(gk.s, P.aw[q][i], MAGIC64));
+              den[q] = mad_wide(wc, F[0], den[q]);
+              den[q] = mad_wide(wsn, F[1], den[q]);
+              num[q] = mad_wide(wc, F[2], num[q]);
+              num[q] = mad_wide(wsn, F[3], num[q]);
+            }
+          }
           if ((i & 7) == 7 || (FULL ? i + 1 == MAXK : i + 1 == P.nk)) bar_arrive(BAR_U_EMPTY + 2 * b + (i >> 3), n_uempty);
         }
       }
-      if (act) finish_pixel(P, num, den, Ic, prow + (long long)y * P.W, out, ws);
+      if (act) {
+#pragma unroll
+        for (int q = 0; q < NPL; ++q)
+          if (q == 0 || q < P.nplans) finish_pixel(P, num[q], den[q], Ic, prow + (long long)y * P.W + q * P.plan_stride, out, ws);
+      }
     }
   }
 }
@@ -1433,8 +1443,8 @@ template <int MAXK, int FORM, bool U8, int NT, bool CONSEC, bool FULL = false, b
 cudaError_t launch_one(KParams P, const void* in, float* out, longlong2* ws, dim3 grid, cudaStream_t st, int kern) {
   if constexpr (NT == WS_V && FORM != 4) {
     if (kern == KERN_WS2) {
-      if constexpr (!MULTI && FORM != 5) {
-        auto kfn = bf_ws2_kernel<MAXK, FORM, U8, CONSEC, FULL>;
+      if constexpr (FORM != 5) {
+        auto kfn = bf_ws2_kernel<MAXK, FORM, U8, CONSEC, FULL, MULTI>;
         const size_t smem = smem_layout_ws2(P, U8);
         if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
         cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1722,7 +1732,7 @@ bf_status run_filter(const bf_plan* const* plans, int nplans, const void* d_in, 
       }
     if (ok && m <= 2 && r0 == rlo && (m == 1 || r1 <= r0)) wpar = (m == 2) ? ((r0 - r1) & 1) : 0;
   }
-  if (nplans > 1) sh.kern = KERN_BAND;            // Case 1 multi-plan combine: band kernel (measured faster)
+  if (nplans > 1 && sh.kern != KERN_WS2) sh.kern = KERN_BAND;   // Case 1 multi-plan combine: kernel 2b or 1
   if (sh.kern == KERN_WS && wpar < 0) sh.kern = KERN_BAND;
   if ((4 * std::min(sh.MAXK, p->n_k) + 31) / 32 > 2) sh.kern = KERN_BAND;   // two scan warps
   const int halo = rlo + rhi;
