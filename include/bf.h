@@ -18,7 +18,9 @@
  *     a_k cos(w_k I(x)), a_k sin(w_k I(x)) (Q17); out = num / den.
  *
  * All functions are thread-safe. A plan is immutable after creation and may be used
- * concurrently by several bf_apply calls on different streams.
+ * concurrently by several bf_apply calls on different streams. No device-side entry point
+ * allocates device memory or synchronises the host (bf_apply_host excepted, see there), so every
+ * bf_apply* call can be captured into a CUDA graph.
  */
 #ifndef BF_H_
 #define BF_H_
@@ -48,7 +50,9 @@ typedef enum {
   BF_ERR_UNSUPPORTED = 2,   /* unknown kernel kind, or a plan shape the GPU path lacks       */
   BF_ERR_NO_MEMORY = 3,     /* host allocation failed                                        */
   BF_ERR_CUDA = 4,          /* a CUDA launch or runtime call failed (no device sync is done)  */
-  BF_ERR_NUMERIC = 5        /* the fitter produced no usable term (e.g. all coefficients 0)  */
+  BF_ERR_NUMERIC = 5,       /* the fitter produced no usable term (e.g. all coefficients 0)  */
+  BF_ERR_WORKSPACE = 6      /* the plan runs in several passes and needs a device workspace:
+                               pass one through bf_apply_ex (size: bf_workspace_size)         */
 } bf_status;
 
 /* Spatial kernel K_s: isotropic Gaussian exp(-(u^2+v^2)/2 sigma_s^2) or a box,
@@ -149,9 +153,64 @@ BF_API bf_status bf_plan_get_info(const bf_plan* plan, bf_plan_info* info);
  * deterministic (fixed reduction order, exact integer box sums, no atomics).
  * Returns BF_ERR_INVALID_ARG for NULL pointers, H or W <= 0, H*W overflow or d_in == d_out;
  * BF_ERR_UNSUPPORTED if the plan's spatial kernel has no box-pair form of rank <= 2 (see
- * bf_plan_info.spatial_rank; rank 2 is K~_s = sum_{s<2} fx_s(u) fy_s(v) with box factors).
+ * bf_plan_info.spatial_rank; rank 2 is K~_s = sum_{s<2} fx_s(u) fy_s(v) with box factors);
+ * BF_ERR_WORKSPACE if the plan runs in several passes (rank-2 or >= 3-box plans with more than 8
+ * or 16 terms; every separable N_s = 9 / box plan with N <= 32 runs in one pass): use bf_apply_ex.
  */
 BF_API bf_status bf_apply(const bf_plan* plan, const void* d_in, float* d_out, int H, int W, bf_stream stream);
+
+/* Kernel choice of bf_apply_ex (bf_apply_args.kernel). AUTO is the library's choice; the others
+ * force one kernel where it can run the plan (for A/B timing and the bitwise cross-kernel tests:
+ * all of them compute the same integers). */
+enum { BF_KERNEL_AUTO = 0, BF_KERNEL_BAND = 1, BF_KERNEL_WS = 2, BF_KERNEL_WS2 = 3, BF_KERNEL_WS2_WIDE = 4 };
+/* (BF_KERNEL_WS2_WIDE: kernel 2b with two columns per vertical-pass thread and 8 terms per CTA,
+ * the range terms split over a CTA cluster: the automatic choice for radii above 96) */
+
+/* Optional arguments of bf_apply_ex / bf_workspace_size / bf_apply_config. Zero-initialised (or
+ * bf_apply_args_default) means: library's kernel and tiling, all rows, no workspace, no counters. */
+typedef struct {
+  int kernel;                           /* BF_KERNEL_*                                             */
+  int band_rows;                        /* output rows per CTA band; 0 = the library's cost model  */
+  int row_begin, row_end;               /* compute output rows [row_begin, row_end) only (the input
+                                           rows their windows need must be valid); 0, 0 = all     */
+  void* d_workspace;                    /* device workspace of multi-pass plans, or NULL           */
+  size_t workspace_bytes;               /* its size (>= bf_workspace_size)                         */
+  unsigned long long* d_fallback_count; /* device counter, or NULL: incremented by the number of
+                                           pixels whose approximated denominator is <= 0 (out =
+                                           I(x), Q18; "the pixel is counted")                 */
+  unsigned char* d_fallback_mask;       /* device n_frames*H*W bytes, or NULL: 1 where the pixel
+                                           took that fallback, else 0                               */
+  double repair_threshold;              /* pixels whose den / sum K~_s (the clipped spatial mass) is
+                                           below this (or den <= 0) are re-evaluated in fp64 from the
+                                           approximated kernels (the direct double loop, reading Q27):
+                                           0 = the library default (BF_REPAIR_DEFAULT), < 0 = off     */
+  int u8_trig;                          /* u8 plans: 0 = the base angles (cos, sin)(pi I / D) from a
+                                           256-entry table (Case 2; default), 1 = evaluated
+                                           per tap (kernel 1 only): the same values, bitwise the same
+                                           output                                            */
+} bf_apply_args;
+
+/* Default bf_apply_args.repair_threshold: out = num / den magnifies the integer format's rounding
+ * (relative ~1e-8 of the full-window denominator) by 1 / cond; below cond = 0.015 that can reach
+ * the 1e-3 parity tolerance on the [0, 255] scale (measured on BASELINE cfg4 at 8192^2). At most
+ * 65536 flagged pixels per call are repaired; up to 16 calls may be in flight per device. */
+#define BF_REPAIR_DEFAULT 0.015
+
+BF_API void bf_apply_args_default(bf_apply_args* args);
+
+/*
+ * bf_apply / bf_apply_batched with optional arguments (args may be NULL). Same contract as
+ * bf_apply: asynchronous on `stream`, no allocation, no host synchronisation, graph capturable.
+ * Multi-pass plans accumulate num / den (int64) in args->d_workspace (BF_ERR_WORKSPACE if it is
+ * missing or too small); the counter / mask are written by the launch that finishes the pixel.
+ */
+BF_API bf_status bf_apply_ex(const bf_plan* plan, const void* d_in, float* d_out, int n_frames, int H, int W,
+                             bf_stream stream, const bf_apply_args* args);
+
+/* Device workspace bytes bf_apply_ex needs for this plan, shape and kernel choice (0 for one-pass
+ * plans). Pure host computation. */
+BF_API bf_status bf_workspace_size(const bf_plan* plan, int n_frames, int H, int W, const bf_apply_args* args,
+                                   size_t* bytes);
 
 /*
  * Filters n_frames independent H x W frames stored back to back (frame f at d_in + f*H*W
@@ -166,9 +225,11 @@ BF_API bf_status bf_apply_batched(const bf_plan* plan, const void* d_in, float* 
  * plans (e.g. several sigma_r, or Gaussian and Tukey) are evaluated in ONE pass that shares the
  * vertical / horizontal box filtering; only the per-pixel combine runs per plan.
  * plans[0..n_plans) must share the spatial plan (same boxes and weights), D and input dtype
- * (else BF_ERR_INVALID_ARG); the union of their selected k must fit one pass (<= 16 terms, else
- * BF_ERR_UNSUPPORTED). d_out holds n_plans H x W float32 images back to back (plan q at
- * d_out + q*H*W). 1 <= n_plans <= BF_MAX_PLANS. Otherwise as bf_apply.
+ * (else BF_ERR_INVALID_ARG); the union of their selected k must fit one CTA's pass (<= 16 terms)
+ * and the spatial plan must be separable with at most two boxes per axis (the default N_s = 9,
+ * or a box), else BF_ERR_UNSUPPORTED. d_out holds n_plans H x W float32 images back to back (plan
+ * q at d_out + q*H*W). 1 <= n_plans <= BF_MAX_PLANS. Otherwise as bf_apply. For range plans not
+ * known up front use bf_precompute / bf_apply_cached below.
  */
 BF_API bf_status bf_apply_multi(const bf_plan* const* plans, int n_plans, const void* d_in, float* d_out, int H, int W,
                                 bf_stream stream);
@@ -178,14 +239,16 @@ BF_API bf_status bf_apply_multi(const bf_plan* const* plans, int n_plans, const 
  * five row chunks pipelined over library-owned streams (ordered after the work already in
  * `stream`): the copy of the next input piece, the filter of the current chunk and the copy back
  * of the previous chunk overlap. Pinned host buffers make the copies asynchronous. Device
- * buffers come from a library-owned cache keyed by size (grown on demand, freed at exit; one
- * device per process). Results equal bf_apply's bitwise. */
+ * buffers (input, output and, for multi-pass plans, the workspace) come from a library-owned
+ * cache per device (grown on demand, freed at exit); calls on different devices run
+ * concurrently, calls on one device are serialised. This is the one entry point that allocates
+ * device memory and synchronises (`stream`, before returning). Results equal bf_apply's bitwise. */
 BF_API bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float* h_out, int H, int W, bf_stream stream);
 
 /*
  * Number of kernel launches one bf_apply / bf_apply_batched of an H x W image enqueues with this
- * plan (the range terms run in ceil(N_eff / terms-per-pass) passes; several passes accumulate
- * num / den in an int64 workspace). Pure host computation, no device work. Returns
+ * plan (1, or ceil(N_eff / terms-per-pass) passes for multi-pass plans, which accumulate num /
+ * den in the caller's workspace). Pure host computation, no device work. Returns
  * BF_ERR_INVALID_ARG for a NULL plan / pointer or H, W <= 0, BF_ERR_UNSUPPORTED as bf_apply would.
  */
 BF_API bf_status bf_apply_launches(const bf_plan* plan, int H, int W, int* n_launches);
@@ -200,12 +263,45 @@ typedef struct bf_launch_config {
   int n_launches;
   const char* kernel;
   int threads_per_cta;
-  int grid_x, grid_y, grid_z;
+  int grid_x, grid_y, grid_z;    /* grid_x counts every CTA: strips x cluster_size          */
   int tile_w, tile_h;
   size_t smem_bytes;
+  int cluster_size;              /* CTAs per cluster (range terms split over the cluster)    */
+  int terms_per_cta;             /* range terms one CTA evaluates per pass                   */
+  int cols_per_thread;           /* extended columns per vertical-pass thread (kernel 2b)    */
+  size_t workspace_bytes;        /* bf_workspace_size of the same call                       */
 } bf_launch_config;
 
-BF_API bf_status bf_apply_config(const bf_plan* plan, int n_frames, int H, int W, bf_launch_config* cfg);
+/* args may be NULL (as bf_apply); args->kernel / band_rows are honoured as in bf_apply_ex. */
+BF_API bf_status bf_apply_config(const bf_plan* plan, int n_frames, int H, int W, const bf_apply_args* args,
+                                 bf_launch_config* cfg);
+
+/*
+ * Case 1 of the paper's pre-computation (NEXT f2), the paper's two phases:
+ * bf_precompute runs once per image and stores the box-filtered channels of the frequencies
+ * k = 0 .. k_count-1 (4 int32 planes per k: S(g^c_k), S(g^s_k), S(G^c_k), S(G^s_k) of
+ * eq:numerator_2D_box_N_terms; with T_{r_i} = D they do not depend on the range kernel,
+ * P:1205) in the caller's device buffer d_cache (bf_cache_size bytes; layout plane
+ * 4k + c of H*W int32, row-major). bf_apply_cached then evaluates any range plan whose selected
+ * k all lie below k_count and whose spatial plan, D and input dtype equal the precompute plan's,
+ * as one combine-only pass that reads the cache and the input (HBM-bound); its output equals
+ * bf_apply's bitwise. Both are asynchronous on `stream`, allocate nothing and are graph
+ * capturable. desc (host memory, filled by bf_precompute) carries what bf_apply_cached checks.
+ * Errors: BF_ERR_INVALID_ARG for NULL pointers, sizes, k_count outside [1, BF_MAX_TERMS], a too
+ * small cache, or a plan that does not match desc; BF_ERR_UNSUPPORTED for literal plans and
+ * spatial plans other than separable with at most two boxes per axis.
+ */
+typedef struct {
+  int k_count, H, W, input_dtype;
+  double intensity_max;
+  unsigned long long spatial_key;   /* fingerprint of the spatial plan and the channel quantisation */
+} bf_cache_desc;
+
+BF_API bf_status bf_cache_size(const bf_plan* plan, int k_count, int H, int W, size_t* bytes);
+BF_API bf_status bf_precompute(const bf_plan* plan, int k_count, const void* d_in, int H, int W, void* d_cache,
+                               size_t cache_bytes, bf_stream stream, bf_cache_desc* desc);
+BF_API bf_status bf_apply_cached(const bf_plan* plan, const bf_cache_desc* desc, const void* d_cache,
+                                 const void* d_in, float* d_out, bf_stream stream, const bf_apply_args* args);
 
 /* Static string for a status code. */
 BF_API const char* bf_status_string(bf_status s);

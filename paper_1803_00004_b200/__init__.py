@@ -10,10 +10,12 @@ streams; every step of the filter runs in the library's host fitter and sm_100a 
 """
 from __future__ import annotations
 
-from ._bf import (BFError, Plan, apply, apply_batched, apply_host, apply_multi, config, launches, lib, version)
+from ._bf import (BFError, CacheDesc, Plan, apply, apply_batched, apply_cached, apply_ex, apply_host, apply_multi,
+                  cache_size, config, launches, lib, make_args, precompute, version, workspace_size)
 
-__all__ = ["BFError", "Plan", "apply", "apply_batched", "apply_host", "apply_multi", "bilateral_filter",
-           "bilateral_filter_multi", "config", "launches", "lib", "version"]
+__all__ = ["BFError", "CacheDesc", "Plan", "apply", "apply_batched", "apply_cached", "apply_ex", "apply_host",
+           "apply_multi", "bilateral_filter", "bilateral_filter_multi", "cache_size", "config", "launches", "lib",
+           "make_args", "precompute", "version", "workspace_size", "RangeCache"]
 
 
 def _check_tensor(t, plan):
@@ -27,20 +29,64 @@ def _check_tensor(t, plan):
         raise ValueError("input must be contiguous (row-major, pitch W)")
 
 
-def bilateral_filter(plan: Plan, img, out=None, stream=None):
-    """Filters a [H, W] (or [F, H, W] batch) CUDA tensor with `plan` on the current stream."""
+def bilateral_filter(plan: Plan, img, out=None, stream=None, kernel: str = "auto", band_rows: int = 0,
+                     fallback_count=None, fallback_mask=None, repair_threshold: float = 0.0, u8_trig: str = "lut"):
+    """Filters a [H, W] (or [F, H, W] batch) CUDA tensor with `plan` on the current stream.
+
+    Multi-pass plans get a workspace from torch's allocator (the caller's memory: the library
+    itself never allocates). fallback_count: optional int64 CUDA tensor [1] incremented by the
+    number of pixels whose denominator was <= 0 (out = I(x)); fallback_mask: optional uint8 CUDA
+    tensor shaped like img (1 there, else 0). repair_threshold: see bf_apply_args (0 = default,
+    < 0 = no fp64 repair of ill-conditioned pixels)."""
     import torch
     _check_tensor(img, plan)
+    if img.dim() not in (2, 3):
+        raise ValueError("expected [H, W] or [F, H, W]")
     if out is None:
         out = torch.empty(img.shape, dtype=torch.float32, device=img.device)
     s = (stream or torch.cuda.current_stream(img.device)).cuda_stream
-    if img.dim() == 2:
-        apply(plan, img.data_ptr(), out.data_ptr(), img.shape[0], img.shape[1], s)
-    elif img.dim() == 3:
-        apply_batched(plan, img.data_ptr(), out.data_ptr(), img.shape[0], img.shape[1], img.shape[2], s)
-    else:
-        raise ValueError("expected [H, W] or [F, H, W]")
+    F, H, W = (1,) + tuple(img.shape) if img.dim() == 2 else tuple(img.shape)
+    args = make_args(kernel=kernel, band_rows=band_rows,
+                     fallback_count=fallback_count.data_ptr() if fallback_count is not None else 0,
+                     fallback_mask=fallback_mask.data_ptr() if fallback_mask is not None else 0,
+                     repair_threshold=repair_threshold, u8_trig=u8_trig)
+    ws = workspace_size(plan, H, W, F, args)
+    wst = None
+    if ws:
+        wst = torch.empty(ws, dtype=torch.uint8, device=img.device)
+        args.d_workspace = wst.data_ptr()
+        args.workspace_bytes = ws
+    apply_ex(plan, img.data_ptr(), out.data_ptr(), F, H, W, s, args)
+    if wst is not None:
+        wst.record_stream(stream or torch.cuda.current_stream(img.device))
     return out
+
+
+class RangeCache:
+    """Case 1 of the paper's pre-computation on a [H, W] CUDA tensor: the box-filtered
+    channels of k = 0 .. k_count-1 are computed once (bf_precompute); any range plan sharing the
+    spatial plan is then applied by a combine-only pass (bf_apply_cached), bitwise equal to
+    bilateral_filter. The cache is a torch CUDA tensor (4 * k_count * H * W int32)."""
+
+    def __init__(self, plan: Plan, img, k_count: int, stream=None):
+        import torch
+        _check_tensor(img, plan)
+        if img.dim() != 2:
+            raise ValueError("expected [H, W]")
+        self.img = img
+        H, W = img.shape
+        n = cache_size(plan, k_count, H, W)
+        self.buf = torch.empty(n, dtype=torch.uint8, device=img.device)
+        s = (stream or torch.cuda.current_stream(img.device)).cuda_stream
+        self.desc = precompute(plan, k_count, img.data_ptr(), H, W, self.buf.data_ptr(), n, s)
+
+    def apply(self, plan: Plan, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty(self.img.shape, dtype=torch.float32, device=self.img.device)
+        s = (stream or torch.cuda.current_stream(self.img.device)).cuda_stream
+        apply_cached(plan, self.desc, self.buf.data_ptr(), self.img.data_ptr(), out.data_ptr(), s)
+        return out
 
 
 def bilateral_filter_multi(plans, img, stream=None):

@@ -10,7 +10,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbf.so")
 
-BF_OK, BF_ERR_INVALID_ARG, BF_ERR_UNSUPPORTED, BF_ERR_NO_MEMORY, BF_ERR_CUDA, BF_ERR_NUMERIC = range(6)
+BF_OK, BF_ERR_INVALID_ARG, BF_ERR_UNSUPPORTED, BF_ERR_NO_MEMORY, BF_ERR_CUDA, BF_ERR_NUMERIC, BF_ERR_WORKSPACE = range(7)
+KERNELS = {"auto": 0, "band": 1, "ws": 2, "ws2": 3, "ws2wide": 4}
 BF_SPATIAL_GAUSSIAN, BF_SPATIAL_BOX = 0, 1
 BF_RANGE_GAUSSIAN, BF_RANGE_TUKEY = 0, 1
 BF_IN_U8, BF_IN_F32 = 0, 1
@@ -23,8 +24,9 @@ RANGE = {"gaussian": BF_RANGE_GAUSSIAN, "tukey": BF_RANGE_TUKEY}
 
 #: every symbol include/bf.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bf_plan_options_default", "bf_plan_create", "bf_plan_destroy", "bf_plan_get_info", "bf_apply",
-           "bf_apply_batched", "bf_apply_config", "bf_apply_host", "bf_apply_launches", "bf_apply_multi",
-           "bf_status_string", "bf_version")
+           "bf_apply_args_default", "bf_apply_ex", "bf_workspace_size", "bf_apply_batched", "bf_apply_config",
+           "bf_apply_host", "bf_apply_launches", "bf_apply_multi", "bf_cache_size", "bf_precompute",
+           "bf_apply_cached", "bf_status_string", "bf_version")
 BF_MAX_PLANS = 4
 
 
@@ -36,7 +38,20 @@ class PlanOptions(C.Structure):
 class LaunchConfig(C.Structure):
     _fields_ = [("n_launches", C.c_int), ("kernel", C.c_char_p), ("threads_per_cta", C.c_int), ("grid_x", C.c_int),
                 ("grid_y", C.c_int), ("grid_z", C.c_int), ("tile_w", C.c_int), ("tile_h", C.c_int),
-                ("smem_bytes", C.c_size_t)]
+                ("smem_bytes", C.c_size_t), ("cluster_size", C.c_int), ("terms_per_cta", C.c_int),
+                ("cols_per_thread", C.c_int), ("workspace_bytes", C.c_size_t)]
+
+
+class ApplyArgs(C.Structure):
+    _fields_ = [("kernel", C.c_int), ("band_rows", C.c_int), ("row_begin", C.c_int), ("row_end", C.c_int),
+                ("d_workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+                ("d_fallback_count", C.c_void_p), ("d_fallback_mask", C.c_void_p), ("repair_threshold", C.c_double),
+                ("u8_trig", C.c_int)]
+
+
+class CacheDesc(C.Structure):
+    _fields_ = [("k_count", C.c_int), ("H", C.c_int), ("W", C.c_int), ("input_dtype", C.c_int),
+                ("intensity_max", C.c_double), ("spatial_key", C.c_ulonglong)]
 
 
 class PlanInfo(C.Structure):
@@ -93,8 +108,20 @@ def lib() -> C.CDLL:
         L.bf_apply_multi.restype = C.c_int
         L.bf_apply_launches.argtypes = [P, C.c_int, C.c_int, C.POINTER(C.c_int)]
         L.bf_apply_launches.restype = C.c_int
-        L.bf_apply_config.argtypes = [P, C.c_int, C.c_int, C.c_int, C.POINTER(LaunchConfig)]
+        L.bf_apply_config.argtypes = [P, C.c_int, C.c_int, C.c_int, C.POINTER(ApplyArgs), C.POINTER(LaunchConfig)]
         L.bf_apply_config.restype = C.c_int
+        L.bf_apply_args_default.argtypes = [C.POINTER(ApplyArgs)]
+        L.bf_apply_args_default.restype = None
+        L.bf_apply_ex.argtypes = [P, P, P, C.c_int, C.c_int, C.c_int, P, C.POINTER(ApplyArgs)]
+        L.bf_apply_ex.restype = C.c_int
+        L.bf_workspace_size.argtypes = [P, C.c_int, C.c_int, C.c_int, C.POINTER(ApplyArgs), C.POINTER(C.c_size_t)]
+        L.bf_workspace_size.restype = C.c_int
+        L.bf_cache_size.argtypes = [P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_size_t)]
+        L.bf_cache_size.restype = C.c_int
+        L.bf_precompute.argtypes = [P, C.c_int, P, C.c_int, C.c_int, P, C.c_size_t, P, C.POINTER(CacheDesc)]
+        L.bf_precompute.restype = C.c_int
+        L.bf_apply_cached.argtypes = [P, C.POINTER(CacheDesc), P, P, P, P, C.POINTER(ApplyArgs)]
+        L.bf_apply_cached.restype = C.c_int
         L.bf_status_string.argtypes = [C.c_int]
         L.bf_status_string.restype = C.c_char_p
         L.bf_version.argtypes = []
@@ -162,10 +189,66 @@ class Plan:
             pass
 
 
+def make_args(kernel: str = "auto", band_rows: int = 0, rows=None, workspace=(0, 0), fallback_count: int = 0,
+              fallback_mask: int = 0, repair_threshold: float = 0.0, u8_trig: str = "lut") -> ApplyArgs:
+    """bf_apply_args: kernel choice, band height, output row range, workspace (ptr, bytes), device
+    fallback counter / mask pointers (0 = off), fp64 repair threshold (0 = default, < 0 = off)."""
+    a = ApplyArgs()
+    lib().bf_apply_args_default(C.byref(a))
+    a.kernel = KERNELS[kernel]
+    a.band_rows = int(band_rows)
+    if rows is not None:
+        a.row_begin, a.row_end = int(rows[0]), int(rows[1])
+    a.d_workspace = C.c_void_p(int(workspace[0])) if workspace[0] else None
+    a.workspace_bytes = int(workspace[1])
+    a.d_fallback_count = C.c_void_p(int(fallback_count)) if fallback_count else None
+    a.d_fallback_mask = C.c_void_p(int(fallback_mask)) if fallback_mask else None
+    a.repair_threshold = float(repair_threshold)
+    a.u8_trig = {"lut": 0, "direct": 1}[u8_trig]
+    return a
+
+
 def apply(plan: Plan, d_in: int, d_out: int, H: int, W: int, stream: int = 0) -> None:
     """bf_apply on raw device pointers (ints) and a raw cudaStream_t (int)."""
     _check(lib().bf_apply(plan.handle, C.c_void_p(d_in), C.c_void_p(d_out), int(H), int(W), C.c_void_p(stream)),
            "bf_apply")
+
+
+def apply_ex(plan: Plan, d_in: int, d_out: int, n_frames: int, H: int, W: int, stream: int = 0,
+             args: ApplyArgs | None = None) -> None:
+    """bf_apply_ex (optional arguments: see make_args)."""
+    _check(lib().bf_apply_ex(plan.handle, C.c_void_p(d_in), C.c_void_p(d_out), int(n_frames), int(H), int(W),
+                             C.c_void_p(stream), C.byref(args) if args is not None else None), "bf_apply_ex")
+
+
+def workspace_size(plan: Plan, H: int, W: int, n_frames: int = 1, args: ApplyArgs | None = None) -> int:
+    n = C.c_size_t(0)
+    _check(lib().bf_workspace_size(plan.handle, int(n_frames), int(H), int(W),
+                                   C.byref(args) if args is not None else None, C.byref(n)), "bf_workspace_size")
+    return n.value
+
+
+def cache_size(plan: Plan, k_count: int, H: int, W: int) -> int:
+    n = C.c_size_t(0)
+    _check(lib().bf_cache_size(plan.handle, int(k_count), int(H), int(W), C.byref(n)), "bf_cache_size")
+    return n.value
+
+
+def precompute(plan: Plan, k_count: int, d_in: int, H: int, W: int, d_cache: int, cache_bytes: int,
+               stream: int = 0) -> CacheDesc:
+    """bf_precompute (Case 1, phase 1): box-filtered channels of k = 0 .. k_count-1 into d_cache."""
+    d = CacheDesc()
+    _check(lib().bf_precompute(plan.handle, int(k_count), C.c_void_p(d_in), int(H), int(W), C.c_void_p(d_cache),
+                               int(cache_bytes), C.c_void_p(stream), C.byref(d)), "bf_precompute")
+    return d
+
+
+def apply_cached(plan: Plan, desc: CacheDesc, d_cache: int, d_in: int, d_out: int, stream: int = 0,
+                 args: ApplyArgs | None = None) -> None:
+    """bf_apply_cached (Case 1, phase 2): combine-only pass of a range plan over the cache."""
+    _check(lib().bf_apply_cached(plan.handle, C.byref(desc), C.c_void_p(d_cache), C.c_void_p(d_in),
+                                 C.c_void_p(d_out), C.c_void_p(stream), C.byref(args) if args is not None else None),
+           "bf_apply_cached")
 
 
 def apply_batched(plan: Plan, d_in: int, d_out: int, n_frames: int, H: int, W: int, stream: int = 0) -> None:
@@ -194,13 +277,17 @@ def launches(plan: Plan, H: int, W: int) -> int:
     return n.value
 
 
-def config(plan: Plan, H: int, W: int, n_frames: int = 1) -> dict:
-    """Launch configuration of bf_apply(_batched) for this shape (bf_apply_config): kernel name,
-    threads per CTA, grid, output tile, dynamic shared memory, launches."""
+def config(plan: Plan, H: int, W: int, n_frames: int = 1, args: ApplyArgs | None = None) -> dict:
+    """Launch configuration of bf_apply(_ex) for this shape (bf_apply_config): kernel name,
+    threads per CTA, grid, output tile, dynamic shared memory, launches, cluster size, terms per
+    CTA, columns per vertical-pass thread, workspace bytes."""
     c = LaunchConfig()
-    _check(lib().bf_apply_config(plan.handle, int(n_frames), int(H), int(W), C.byref(c)), "bf_apply_config")
+    _check(lib().bf_apply_config(plan.handle, int(n_frames), int(H), int(W),
+                                 C.byref(args) if args is not None else None, C.byref(c)), "bf_apply_config")
     return {"kernel": c.kernel.decode(), "launches": c.n_launches, "threads_per_cta": c.threads_per_cta,
-            "grid": (c.grid_x, c.grid_y, c.grid_z), "tile": (c.tile_w, c.tile_h), "smem_bytes": c.smem_bytes}
+            "grid": (c.grid_x, c.grid_y, c.grid_z), "tile": (c.tile_w, c.tile_h), "smem_bytes": c.smem_bytes,
+            "cluster": c.cluster_size, "terms_per_cta": c.terms_per_cta, "cols_per_thread": c.cols_per_thread,
+            "workspace_bytes": c.workspace_bytes}
 
 
 def version() -> str:

@@ -1,0 +1,1047 @@
+// Host side of libbf.so's apply calls: plan shapes, launch shapes (cost model), parameter blocks,
+// the C-ABI entry points (bf_apply*, bf_precompute / bf_apply_cached, bf_apply_host).
+//
+// Nothing here allocates device memory except bf_apply_host's per-device buffer cache: multi-pass
+// plans use the caller's workspace (bf_apply_ex), the literal kernel's table travels by value in
+// the kernel parameters, so every device entry point is CUDA-graph capturable.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "bf_params.h"
+
+using namespace bf;
+
+namespace {
+
+constexpr int QBITS_MAX = 22;   // channel quantisation (the FFMA trick's range)
+constexpr int ABITS = 30;       // horizontal integer box weights (F = round(sum H ax / 2^32))
+constexpr int MAX_DEV = 64;
+
+int sm_count() {
+  static std::atomic<int> cache[MAX_DEV];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAX_DEV) {
+    cudaGetLastError();
+    return 148;
+  }
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n > 0) return n;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = 148;
+  }
+  cache[dev].store(n, std::memory_order_relaxed);
+  return n;
+}
+
+// Resident clusters of G kernel-2b CTAs (cached per device, G and column mode); an estimate from the
+// GPC sizes when the device cannot be asked (B200: 148 SMs in GPCs of 16-20; clusters of 4 strand
+// 16 SMs, of 3 about 7).
+int max_clusters(const LaunchSpec& s, size_t smem, int G) {
+  if (G <= 1) return sm_count();
+  static std::atomic<int> cache[MAX_DEV][5][3][2];
+  int dev = 0;
+  const bool have = cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < MAX_DEV;
+  if (!have) cudaGetLastError();
+  const int ci = std::min(s.COLS, 2), ui = s.U8 ? 1 : 0;
+  int n = have ? cache[dev][G][ci][ui].load(std::memory_order_relaxed) : 0;
+  if (n > 0) return n;
+  if (have) n = ws2_max_clusters(s, smem, G);
+  if (n <= 0) {
+    const int nsm = sm_count();
+    n = G == 2 ? nsm / 2 : (G == 3 ? nsm * 141 / 148 / 3 : nsm * 132 / 148 / 4);
+  } else if (have) {
+    cache[dev][G][ci][ui].store(n, std::memory_order_relaxed);
+  }
+  return std::max(1, n);
+}
+
+// Plans that can share one pass of box-filtered channels: same spatial form, D and input type.
+bool same_channels(const bf_plan* a, const bf_plan* b) {
+  if (a->ns != b->ns || a->D != b->D || a->input_dtype != b->input_dtype) return false;
+  for (int t = 0; t < a->ns; ++t) {
+    if (a->snbx[t] != b->snbx[t] || a->snby[t] != b->snby[t]) return false;
+    for (int i = 0; i < a->snbx[t]; ++i)
+      if (a->slox[t][i] != b->slox[t][i] || a->shix[t][i] != b->shix[t][i] || a->swx[t][i] != b->swx[t][i])
+        return false;
+    for (int i = 0; i < a->snby[t]; ++i)
+      if (a->sloy[t][i] != b->sloy[t][i] || a->shiy[t][i] != b->shiy[t][i] || a->swy[t][i] != b->swy[t][i])
+        return false;
+  }
+  return true;
+}
+
+// Spatial form of the plan's GPU box-pair representation: 1 one box, 2 separable <= 2 boxes per
+// axis, 4 separable <= 4, 5 rank 2; 0 = none. rlo / rhi: the horizontal halo.
+int plan_form(const bf_plan* p, int& rlo, int& rhi) {
+  rlo = rhi = 0;
+  if (p->ns < 1 || p->ns > 2) return 0;
+  int nbx = 0, nby = p->snby[0];
+  for (int t = 0; t < p->ns; ++t) {
+    if (p->snbx[t] < 1 || p->snbx[t] > MAXB || p->snby[t] != nby) return 0;
+    nbx = std::max(nbx, p->snbx[t]);
+    for (int b = 0; b < p->snbx[t]; ++b) {
+      rlo = std::max(rlo, -p->slox[t][b]);
+      rhi = std::max(rhi, p->shix[t][b]);
+    }
+    for (int b = 0; b < nby; ++b)
+      if (p->sloy[t][b] != p->sloy[0][b] || p->shiy[t][b] != p->shiy[0][b]) return 0;
+  }
+  if (nby < 1 || nby > MAXB) return 0;
+  if (p->ns == 2) return (nbx > 1 || nby > 2) ? 0 : 5;
+  const int nb = std::max(nbx, nby);
+  return nb <= 1 ? 1 : (nb == 2 ? 2 : 4);
+}
+
+// Paired-load layout of the horizontal boxes (kernel 2's walkers): every box symmetric
+// [-r_b, r_b] (odd width), at most two boxes in all, box 0 the widest. -1 = none.
+int paired_layout(const bf_plan* p, int rlo) {
+  int m = 0, r0 = -1, r1 = -1;
+  bool ok = true;
+  for (int t = 0; t < p->ns; ++t)
+    for (int b = 0; b < p->snbx[t]; ++b) {
+      if (p->slox[t][b] != -p->shix[t][b]) ok = false;
+      if (m == 0) r0 = p->shix[t][b];
+      else r1 = p->shix[t][b];
+      ++m;
+    }
+  if (ok && m <= 2 && r0 == rlo && (m == 1 || r1 <= r0)) return (m == 2) ? ((r0 - r1) & 1) : 0;
+  return -1;
+}
+
+// Channel quantisation of the plan (vertical scales, the U' shift, the horizontal integer weights):
+// depends on the spatial plan and D only, so the Case 1 cache can check it by fingerprint.
+void quantise(const bf_plan* p, KParams& P) {
+  const int ns = p->ns;
+  P.ns = ns;
+  P.nby = p->snby[0];
+  double wymax = 0.0;
+  for (int t = 0; t < ns; ++t)
+    for (int b = 0; b < P.nby; ++b) wymax = std::max(wymax, std::fabs(p->swy[t][b]));
+  double wsum = 0.0;
+  for (int t = 0; t < ns; ++t) {
+    double w = 0.0;
+    for (int b = 0; b < P.nby; ++b) w += std::fabs(p->swy[t][b]) / wymax * (p->shiy[t][b] - p->sloy[t][b] + 1);
+    wsum = std::max(wsum, w);
+  }
+  int qb = QBITS_MAX;
+  while (qb > 8 && std::ldexp(wsum, qb) + 4.0 * (p->shiy[0][0] - p->sloy[0][0] + 8) >= 2147483647.0 - 65536.0) --qb;
+  double ubound = 0.0;   // bound of |U_t| before the shift, over the terms
+  P.vmin = p->sloy[0][0];
+  P.vmax = p->shiy[0][0];
+  for (int b = 0; b < P.nby; ++b) {
+    P.vlo[b] = p->sloy[0][b];
+    P.vhi[b] = p->shiy[0][b];
+    P.vmin = std::min(P.vmin, P.vlo[b]);
+    P.vmax = std::max(P.vmax, P.vhi[b]);
+  }
+  for (int t = 0; t < ns; ++t) {
+    double ub = 0.0;
+    for (int b = 0; b < P.nby; ++b) {
+      P.qs[t][b] = (float)std::ldexp(p->swy[t][b] / wymax, qb);
+      P.qsD[t][b] = (float)((double)P.qs[t][b] / p->D);
+      ub += (std::fabs((double)P.qs[t][b]) + 0.5) * (P.vhi[b] - P.vlo[b] + 1);
+    }
+    ubound = std::max(ubound, ub);
+  }
+  // ---- U' = U >> ush: every horizontal box sum H of U' fits int32
+  int nxmax = 1;
+  for (int t = 0; t < ns; ++t)
+    for (int b = 0; b < p->snbx[t]; ++b) nxmax = std::max(nxmax, p->shix[t][b] - p->slox[t][b] + 1);
+  P.ush = 0;
+  while ((ubound / std::ldexp(1.0, P.ush) + 1.0) * nxmax >= 2147483000.0) ++P.ush;
+  P.urnd = P.ush > 0 ? (1 << (P.ush - 1)) : 0;
+  const double uprime = ubound / std::ldexp(1.0, P.ush) + 1.0;
+  // ---- horizontal: integer weights ax = round(wx / max|wx| * 2^abits), F = round(sum H ax / 2^32)
+  //      (one IMAD.WIDE per box into an int64 accumulator, |F - exact| <= 1/2) fits int32
+  double wxmax = 0.0, rw = 0.0;
+  for (int t = 0; t < ns; ++t)
+    for (int b = 0; b < p->snbx[t]; ++b) wxmax = std::max(wxmax, std::fabs(p->swx[t][b]));
+  for (int t = 0; t < ns; ++t)
+    for (int b = 0; b < p->snbx[t]; ++b) rw += std::fabs(p->swx[t][b]) / wxmax * (p->shix[t][b] - p->slox[t][b] + 1);
+  int abits = ABITS;
+  while (abits > 16 && uprime * rw * std::ldexp(1.0, abits - 32) + 8.0 >= 2147483000.0) --abits;
+  for (int t = 0; t < ns; ++t) {
+    P.nbx[t] = p->snbx[t];
+    for (int b = 0; b < p->snbx[t]; ++b) {
+      P.hlo[t][b] = p->slox[t][b];
+      P.hhi[t][b] = p->shix[t][b];
+      P.ax[t][b] = (int)std::lround(std::ldexp(p->swx[t][b] / wxmax, abits));
+    }
+  }
+  const double invD = 1.0 / p->D;
+  P.invD = invD;
+  P.invD_hi = (float)invD;
+  P.invD_lo = (float)(invD - (double)P.invD_hi);
+  P.D = p->D;
+}
+
+// combine weights a_k * 2^wbits: |W| < 2^31 and |num|, |den| < 2^62 for every plan of the call
+int combine_bits(const bf_plan* const* plans, int nplans) {
+  double asum = 0.0, amax = 0.0;
+  for (int q = 0; q < nplans; ++q) {
+    double s1 = 0.0;
+    for (int i = 0; i < plans[q]->n_k; ++i) {
+      s1 += std::fabs(plans[q]->a[i]);
+      amax = std::max(amax, std::fabs(plans[q]->a[i]));
+    }
+    asum = std::max(asum, s1);
+  }
+  int wbits = 29;
+  while (wbits > 8 && (std::ldexp(asum, wbits) * 2.0 * 2147483648.0 >= 4.0e18 || std::ldexp(amax, wbits) >= 2.0e9))
+    --wbits;
+  return wbits;
+}
+
+// F of the k = 0 cosine channel (a constant 1) for an unclipped window: the full spatial mass in
+// the F units of quantise()
+double mass_full(const bf_plan* p, const KParams& P) {
+  double F = 0.0;
+  for (int t = 0; t < P.ns; ++t) {
+    double U = P.urnd;
+    for (int b = 0; b < P.nby; ++b) U += std::rint((double)P.qs[t][b]) * (P.vhi[b] - P.vlo[b] + 1);
+    const double Up = std::floor(U / std::ldexp(1.0, P.ush));
+    for (int b = 0; b < P.nbx[t]; ++b) F += Up * (P.hhi[t][b] - P.hlo[t][b] + 1) * (double)P.ax[t][b];
+  }
+  return F / 4294967296.0;
+}
+
+std::atomic<unsigned> g_repair_ticket{0};
+
+// The repair pass's parameters for the plans of one call (spatial boxes, range terms).
+void repair_params(const bf_plan* const* plans, int nplans, int n_frames, int H, int W, const bf_apply_args& A,
+                   const RepairSink& S, RParams& R) {
+  std::memset(&R, 0, sizeof(R));
+  const bf_plan* p = plans[0];
+  R.H = H;
+  R.W = W;
+  R.frame_elems = (long long)H * W;
+  R.plan_stride = (long long)H * W * n_frames;
+  R.nplans = nplans;
+  R.kmax = 0;
+  for (int q = 0; q < nplans; ++q) {
+    R.nkp[q] = plans[q]->n_k;
+    for (int i = 0; i < plans[q]->n_k; ++i) {
+      R.k[q][i] = plans[q]->k[i];
+      R.a[q][i] = plans[q]->a[i];
+      R.kmax = std::max(R.kmax, plans[q]->k[i]);
+    }
+  }
+  R.D = p->D;
+  R.T = p->T;
+  R.u8 = p->input_dtype == BF_IN_U8;
+  R.ns = p->ns;
+  int rad = 0;
+  for (int s = 0; s < p->ns; ++s) {
+    R.nbx[s] = p->snbx[s];
+    R.nby[s] = p->snby[s];
+    for (int b = 0; b < p->snbx[s]; ++b) {
+      R.lox[s][b] = p->slox[s][b];
+      R.hix[s][b] = p->shix[s][b];
+      R.wx[s][b] = p->swx[s][b];
+      rad = std::max(rad, std::max(-R.lox[s][b], R.hix[s][b]));
+    }
+    for (int b = 0; b < p->snby[s]; ++b) {
+      R.loy[s][b] = p->sloy[s][b];
+      R.hiy[s][b] = p->shiy[s][b];
+      R.wy[s][b] = p->swy[s][b];
+      rad = std::max(rad, std::max(-R.loy[s][b], R.hiy[s][b]));
+    }
+  }
+  R.rad = rad;
+  R.count = S.count;
+  R.list = S.list;
+  R.cap = S.cap;
+  R.fb_count = A.d_fallback_count;
+  R.fb_mask = A.d_fallback_mask;
+}
+
+// Claims a repair slot for one call and clears its counter on the stream (graph capturable).
+bf_status repair_sink(const bf_apply_args& A, double wscale, double mfull, cudaStream_t st, RepairSink& S) {
+  std::memset(&S, 0, sizeof(S));
+  if (A.repair_threshold < 0) return BF_OK;
+  const double tau = A.repair_threshold > 0 ? A.repair_threshold : BF_REPAIR_DEFAULT;
+  const unsigned slot = g_repair_ticket.fetch_add(1, std::memory_order_relaxed) % REPAIR_SLOTS;
+  if (repair_slot(slot, &S.count, &S.list) != cudaSuccess) return BF_ERR_CUDA;
+  if (cudaMemsetAsync(S.count, 0, sizeof(unsigned), st) != cudaSuccess) return BF_ERR_CUDA;
+  S.cap = REPAIR_CAP;
+  S.tau_w = tau * wscale;
+  S.mass_full = mfull;
+  return BF_OK;
+}
+
+// The launches of one call: template choice, parameter block, grid, shared memory, passes.
+struct Launch {
+  LaunchSpec spec;
+  KParams P;
+  dim3 grid;
+  size_t smem = 0;
+  int passes = 1;
+  size_t ws_bytes = 0;
+  const char* name = "";
+  int threads = 0;
+};
+
+size_t smem_band(const KParams& P, int NT, int MAXK, int nk, bool u8, int& f_off, int& l_off) {
+  auto up16 = [](size_t v) { return (v + 15) / 16 * 16; };
+  size_t off = up16(sizeof(int) * P.ns * 4 * (size_t)nk * (NT + 1));
+  f_off = (int)off;
+  off = up16(off + sizeof(int) * (size_t)P.TW * (4 * MAXK + 4));
+  l_off = (int)off;
+  if (u8) off += 256 * (sizeof(float2) + sizeof(double2));
+  return off;
+}
+
+size_t smem_ws(const KParams& P, int MAXK, int nk, bool u8, int& f_off, int& l_off) {
+  auto up16 = [](size_t v) { return (v + 15) / 16 * 16; };
+  size_t off = up16(sizeof(int) * 2 * P.ns * 4 * (size_t)nk * (WS_V + 2));
+  f_off = (int)off;
+  off = up16(off + sizeof(int) * 2 * (size_t)P.TW * (4 * MAXK + 4));
+  l_off = (int)off;
+  if (u8) off += 256 * (sizeof(float2) + sizeof(double2));
+  return off;
+}
+
+// kernel 2b: mbarriers, two U' row buffers of the CTA's channels, LUTs (u8), cluster reduction rows
+size_t smem_ws2(int cols, int nkc, int tw, int G, bool u8, int& l_off, int& r_off) {
+  size_t off = 64 + (sizeof(int) * 2 * 4 * (size_t)nkc * w2_up(cols) + 15) / 16 * 16;
+  l_off = (int)off;
+  if (u8) off += 256 * (sizeof(float2) + sizeof(double2));
+  r_off = (int)off;
+  if (G > 1) off += 2 * (size_t)(G - 1) * tw * sizeof(longlong2);
+  return off;
+}
+
+struct Req {
+  const bf_plan* const* plans;
+  int nplans;
+  int n_frames, H, W;
+  int ya, yb;        // output rows
+  int kernel;        // BF_KERNEL_*
+  int band_rows;     // 0 = cost model
+  bool dump;         // bf_precompute (channels of k = 0 .. nk-1, no combine)
+  bool direct;       // u8: direct trig instead of the Case 2 LUT (kernel 1)
+};
+
+// Chooses kernel, shape and tiling and fills the parameter block (terms of pass 0). Returns
+// BF_OK, BF_ERR_UNSUPPORTED or BF_ERR_INVALID_ARG. No device work (except the cached occupancy
+// query of the cluster launch).
+bf_status prepare(const Req& R, const bf_plan* p, Launch& L) {
+  const int H = R.H, W = R.W, Hr = R.yb - R.ya;
+  int rlo, rhi;
+  const int form = plan_form(p, rlo, rhi);
+  if (form == 0) return BF_ERR_UNSUPPORTED;
+  const int halo = rlo + rhi;
+  const int nk = p->n_k;
+  const bool u8 = p->input_dtype == BF_IN_U8;
+  const int wpar = paired_layout(p, rlo);
+  const bool multi = R.nplans > 1;
+  if (multi && form != 1 && form != 2) return BF_ERR_UNSUPPORTED;
+  std::memset(&L.P, 0, sizeof(L.P));
+  KParams& P = L.P;
+  quantise(p, P);
+  P.H = H;
+  P.W = W;
+  P.yb = R.ya;
+  P.ye = R.yb;
+  P.frame_elems = (long long)H * W;
+  P.rlo_x = rlo;
+  P.nplans = R.nplans;
+  P.plan_stride = (long long)H * W;
+  P.G = 1;
+  bool consec = true;   // CONSEC: the selected k are consecutive
+  for (int i = 1; i < nk; ++i)
+    if (p->k[i] != p->k[i - 1] + 1) consec = false;
+  // ---- kernel choice
+  int kern = KERN_BAND;
+  if (R.kernel == BF_KERNEL_AUTO) kern = (form == 1 || form == 2) ? KERN_WS2 : (form == 5 ? KERN_WS : KERN_BAND);
+  else if (R.kernel == BF_KERNEL_WS2 || R.kernel == BF_KERNEL_WS2_WIDE)
+    kern = (form == 1 || form == 2) ? KERN_WS2 : KERN_BAND;
+  else if (R.kernel == BF_KERNEL_WS) kern = form == 4 ? KERN_BAND : KERN_WS;
+  else if (R.kernel == BF_KERNEL_BAND) kern = KERN_BAND;
+  else return BF_ERR_INVALID_ARG;
+  if (R.dump) kern = KERN_WS2;
+  if (R.direct) {   // Case 2 LUT off: kernel 1's direct-trig instantiation (u8, <= 2 boxes per axis)
+    if (!u8 || (form != 1 && form != 2) || multi || halo + 32 > 256) return BF_ERR_UNSUPPORTED;
+    kern = KERN_BAND;
+  }
+  if (multi && kern == KERN_WS) kern = KERN_BAND;
+  // kernel 2 (NT = 256 class, paired walkers, two scan warps) or fall back to kernel 1
+  if (kern == KERN_WS) {
+    const int maxk = (nk <= 8 || form == 5) ? 8 : 16;
+    if (halo + 32 > WS_V || wpar < 0 || (4 * std::min(maxk, nk) + 31) / 32 > 2) kern = KERN_BAND;
+  }
+  const int nsm = sm_count();
+  const int ry = P.vmax - P.vmin + 1;
+  if (kern == KERN_WS2) {
+    // candidates: (COLS, terms per CTA); G = CTAs per cluster
+    struct Cand {
+      int cols, tpc;
+    } cands[2];
+    int nc = 0;
+    // two columns per thread only where one column leaves strips narrower than 192 outputs (or
+    // when forced: BF_KERNEL_WS2_WIDE)
+    const bool wide_forced = R.kernel == BF_KERNEL_WS2_WIDE;
+    if (halo + 32 <= W2_V && !wide_forced) cands[nc++] = {1, (nk <= 8 && !R.dump) ? 8 : 16};
+    if (halo + 32 <= 2 * W2_V && !multi && !R.dump && (wide_forced || W2_V - halo < 192)) cands[nc++] = {2, 8};
+    double best = -1.0;
+    for (int ci = 0; ci < nc; ++ci) {
+      const int cols = cands[ci].cols, tpc = cands[ci].tpc;
+      const int nterm = R.dump ? std::min(nk, 16) : nk;
+      const int G = (nterm + tpc - 1) / tpc;
+      if (G > 4 || (multi && G > 1) || (R.dump && G > 1)) continue;
+      const int nkc = std::min(tpc, nterm);
+      const int twmax = std::min(w2_nfh(cols), W2_V * cols - halo);
+      LaunchSpec s{};
+      s.kern = KERN_WS2;
+      s.COLS = cols;
+      s.U8 = u8;
+      s.FORM = form;
+      const double ch = 4.0 * nkc / 64.0;
+      for (int tw = twmax; tw >= 1; tw = (tw % 32) ? tw - tw % 32 : tw - 32) {
+        if (tw != twmax && tw < 128) break;
+        int lo, ro;
+        const size_t smem = smem_ws2(cols, nkc, tw, G, u8, lo, ro);
+        if (smem > 227 * 1024) continue;
+        const int wv = (tw + halo + 7) & ~7;
+        // row time: warp-instructions per role (ncu, cfg2, 64 channels: V 694 per 32 extended
+        // columns, FH 942 per 32 outputs, S ~4 per column; V init 373 per 32 columns) at the
+        // measured ~0.55 IPC per SM sub-partition, never below one warp's dependent chain
+        const double row = std::max(6000.0 * ch, ch * (694.0 * ((wv + 31) / 32) + 942.0 * ((tw + 31) / 32) + 4.0 * wv) /
+                                                     (4 * 0.55));
+        const double init = std::max(1500.0 * ch, ch * 373.0 * ((wv + 31) / 32) / (4 * 0.55));
+        const long long strips = (W + tw - 1) / tw;
+        const int slots = G > 1 ? max_clusters(s, smem, G) : nsm;   // resident clusters (CTAs for G = 1)
+        for (int nb = 1; nb <= Hr; ++nb) {
+          const int TH = (Hr + nb - 1) / nb;
+          if (nb > 1 && TH < 16) break;
+          const long long units = strips * nb * R.n_frames;
+          const long long waves = (units + slots - 1) / slots;
+          const double cost = (double)waves * (TH * row + ry * init);
+          if (best < 0 || cost < best * (1.0 - 1e-9)) {
+            best = cost;
+            L.spec = s;
+            L.spec.MAXK = (cols == 2) ? 8 : tpc;
+            P.G = G;
+            P.tpc = tpc;
+            P.TW = tw;
+            P.TH = TH;
+            P.wv = wv;
+            P.l_off = lo;
+            P.r_off = ro;
+            L.smem = smem;
+          }
+        }
+      }
+    }
+    if (best < 0) {
+      if (R.kernel == BF_KERNEL_WS2 || R.kernel == BF_KERNEL_WS2_WIDE || R.dump || multi) return BF_ERR_UNSUPPORTED;
+      kern = KERN_BAND;
+    } else {
+      L.spec.CL = P.G > 1;
+      L.spec.NPL = R.nplans;
+      L.spec.DUMP = R.dump;
+      L.spec.CONSEC = consec;
+      const int nkc0 = std::min(P.tpc, R.dump ? std::min(nk, 16) : nk);
+      L.spec.FULL = R.dump ? (nkc0 == 16) : (P.G > 1 ? (nk % P.tpc == 0 && P.tpc == L.spec.MAXK) : nk == L.spec.MAXK);
+      if (multi) L.spec.FULL = false;
+      L.passes = R.dump ? (nk + 15) / 16 : 1;
+      L.name = "bf_ws2_kernel";
+      L.threads = W2_THREADS;
+      if (R.band_rows > 0) P.TH = std::max(1, std::min(Hr, R.band_rows));
+      const int nb = (Hr + P.TH - 1) / P.TH;
+      L.grid = dim3((unsigned)(((W + P.TW - 1) / P.TW) * P.G), (unsigned)nb, (unsigned)R.n_frames);
+      P.nk = R.dump ? nkc0 : nk;
+      P.ngrp = (4 * nkc0 + 31) / 32;
+      return BF_OK;
+    }
+  }
+  // ---- kernels 1 and 2: NT extended columns, MAXK terms per pass, workspace between passes
+  int NT = 256, MAXK = 8;
+  if (halo <= 128 && halo + 32 <= 256) {
+    NT = 256;
+    MAXK = (nk <= 8 || form == 5) ? 8 : 16;
+  } else {
+    NT = 512;
+    MAXK = (form == 2 && nk > 8) ? 16 : 8;
+    if (kern == KERN_WS) kern = KERN_BAND;
+  }
+  if (halo + 32 > NT) return BF_ERR_UNSUPPORTED;
+  if (form == 5 && (NT != 256 || MAXK != 8)) return BF_ERR_UNSUPPORTED;
+  if (multi && (nk > MAXK)) return BF_ERR_UNSUPPORTED;   // shared channels must fit one pass
+  LaunchSpec& s = L.spec;
+  s = LaunchSpec{};
+  s.kern = kern;
+  s.NT = NT;
+  s.MAXK = MAXK;
+  s.FORM = form;
+  s.U8 = u8;
+  s.NPL = R.nplans;
+  s.COLS = 1;
+  s.DIRECT = R.direct;
+  L.passes = (nk + MAXK - 1) / MAXK;
+  if (L.passes > 1) L.ws_bytes = sizeof(longlong2) * (size_t)H * W * R.n_frames;
+  int TW = NT - halo;
+  P.TW = TW;
+  if (kern == KERN_WS) {   // the double-buffered rows must fit the 227 KB of shared memory
+    int fo, lo;
+    if (smem_ws(P, MAXK, std::min(MAXK, nk), u8, fo, lo) > 227 * 1024) kern = s.kern = KERN_BAND;
+  }
+  const int slots = nsm * ((NT > 256 || kern != KERN_BAND) ? 1 : 2);
+  double best = -1.0;
+  int best_nb = 1;
+  const long long strips = (W + TW - 1) / TW;
+  for (int nb = 1; nb <= Hr; ++nb) {
+    const int TH = (Hr + nb - 1) / nb;
+    if (nb > 1 && TH < 16) break;
+    const long long waves = (strips * nb * R.n_frames + slots - 1) / slots;
+    const double cost = (double)waves * (TH * 4.0 + ry);
+    if (best < 0 || cost < best * (1.0 - 1e-9)) {
+      best = cost;
+      best_nb = nb;
+    }
+  }
+  P.TH = (Hr + best_nb - 1) / best_nb;
+  if (R.band_rows > 0) P.TH = std::max(1, std::min(Hr, R.band_rows));
+  const int nb = (Hr + P.TH - 1) / P.TH;
+  L.grid = dim3((unsigned)strips, (unsigned)nb, (unsigned)R.n_frames);
+  const int nk0 = std::min(MAXK, nk);
+  if (kern == KERN_WS) {
+    L.smem = smem_ws(P, MAXK, nk0, u8, P.f_off, P.l_off);
+    L.name = "bf_ws_kernel";
+    L.threads = WS_THREADS;
+  } else {
+    L.smem = smem_band(P, NT, MAXK, nk0, u8, P.f_off, P.l_off);
+    L.name = "bf_band_kernel";
+    L.threads = NT;
+  }
+  s.CONSEC = consec;
+  s.FULL = false;   // set per pass
+  P.wpar = kern == KERN_WS ? wpar : -1;
+  P.wv = (TW + halo + 7) & ~7;
+  return BF_OK;
+}
+
+// Terms [first, first + n) of plan p (and the multi plans' weights) into the parameter block.
+void set_terms(const Req& R, const bf_plan* p, int first, int n, int wbits, KParams& P) {
+  P.nk = n;
+  for (int i = 0; i < n; ++i) {
+    const int kk = R.dump ? first + i : p->k[first + i];
+    P.kval[i] = kk;
+    P.kstep[i] = i == 0 ? kk : kk - P.kval[i - 1];
+    if (R.dump) continue;
+    if (R.nplans == 1) {
+      P.aw[0][i] = std::ldexp(p->a[first + i], wbits);
+    } else {
+      for (int q = 0; q < R.nplans; ++q) {   // a_k of plan q, 0 where q did not select k
+        double a = 0.0;
+        for (int j = 0; j < R.plans[q]->n_k; ++j)
+          if (R.plans[q]->k[j] == kk) a = R.plans[q]->a[j];
+        P.aw[q][i] = std::ldexp(a, wbits);
+      }
+    }
+  }
+}
+
+cudaError_t dispatch(const LaunchSpec& s, const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid,
+                     size_t smem, cudaStream_t st) {
+  if (s.kern == KERN_WS2) {
+    if (s.CL || s.COLS == 2 || s.DUMP) return launch_ws2_cluster(s, P, in, out, ws, grid, smem, st);
+    if (s.NPL > 1) return s.U8 ? launch_ws2_multi_u8(s, P, in, out, ws, grid, smem, st)
+                               : launch_ws2_multi_f32(s, P, in, out, ws, grid, smem, st);
+    return launch_ws2(s, P, in, out, ws, grid, smem, st);
+  }
+  if (s.kern == KERN_WS) return launch_ws(s, P, in, out, ws, grid, smem, st);
+  return launch_band(s, P, in, out, ws, grid, smem, st);
+}
+
+// ---- the literal-window path (kernel 3): u8 input, levels 0..255 (D = 255), separable plans with
+// at most two boxes per axis whose halo fits the 128-column strip.
+bf_status literal_launch(const bf_plan* p, int n_frames, int H, int W, LParams& Lp, dim3& grid, size_t& smem) {
+  if (p->input_dtype != BF_IN_U8 || p->D != 255.0 || p->ns != 1 || p->snbx[0] > 2 || p->snby[0] > 2)
+    return BF_ERR_UNSUPPORTED;
+  std::memset(&Lp, 0, sizeof(Lp));
+  int rlo = 0, rhi = 0;
+  Lp.nbx = p->snbx[0];
+  Lp.nby = p->snby[0];
+  for (int b = 0; b < Lp.nbx; ++b) {
+    Lp.hlo[b] = p->slox[0][b];
+    Lp.hhi[b] = p->shix[0][b];
+    rlo = std::max(rlo, -Lp.hlo[b]);
+    rhi = std::max(rhi, Lp.hhi[b]);
+  }
+  if (rlo + rhi + 32 > LIT_NT) return BF_ERR_UNSUPPORTED;
+  // the packed 16-bit counts must not overflow: (box height) x (box width) < 2^15
+  for (int b = 0; b < Lp.nby; ++b)
+    if ((long long)(p->shiy[0][b] - p->sloy[0][b] + 1) * (rlo + rhi + 1) >= 32768) return BF_ERR_UNSUPPORTED;
+  Lp.vmin = p->sloy[0][0];
+  Lp.vmax = p->shiy[0][0];
+  for (int b = 0; b < Lp.nby; ++b) {
+    Lp.vlo[b] = p->sloy[0][b];
+    Lp.vhi[b] = p->shiy[0][b];
+    Lp.vmin = std::min(Lp.vmin, Lp.vlo[b]);
+    Lp.vmax = std::max(Lp.vmax, Lp.vhi[b]);
+  }
+  for (int by = 0; by < 2; ++by)
+    for (int bx = 0; bx < 2; ++bx)
+      Lp.wxy[by][bx] = (by < Lp.nby && bx < Lp.nbx) ? p->swy[0][by] * p->swx[0][bx] : 0.0;
+  Lp.H = H;
+  Lp.W = W;
+  Lp.rlo_x = rlo;
+  Lp.TW = LIT_NT - (rlo + rhi);
+  Lp.frame_elems = (long long)H * W;
+  Lp.Tw = (int)std::floor(p->T + 1e-9);
+  // K_lit(t) = sum_k a_k cos(pi k t / T_r) for |t| <= T_r (eq:trigonometric_N_terms), 0 outside
+  // the window, quantised to 2^30: |num|, |den| < 2^63 for |K_lit| < 2
+  for (int t = -255; t <= 255; ++t) {
+    double k = 0.0;
+    if (std::abs(t) <= Lp.Tw)
+      for (int i = 0; i < p->n_k; ++i) k += p->a[i] * std::cos(M_PI * p->k[i] * t / p->T);
+    if (!(std::fabs(k) < 2.0)) return BF_ERR_NUMERIC;
+    Lp.klut[t + 255] = (int)std::lrint(std::ldexp(k, LIT_KB));
+  }
+  const int nstrips = (W + Lp.TW - 1) / Lp.TW;
+  const int nsm = sm_count();
+  const int ry = Lp.vmax - Lp.vmin + 1;
+  long long best_cost = -1;
+  int best_nb = 1;
+  for (int nb = 1; nb <= H; ++nb) {
+    const int TH = (H + nb - 1) / nb;
+    if (nb > 1 && TH < 16) break;
+    const long long ctas = (long long)nstrips * nb * n_frames;
+    const long long waves = (ctas + nsm - 1) / nsm;
+    const long long cost = waves * (4LL * TH + ry);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best_nb = nb;
+    }
+  }
+  Lp.TH = (H + best_nb - 1) / best_nb;
+  grid = dim3(nstrips, (H + Lp.TH - 1) / Lp.TH, n_frames);
+  smem = sizeof(int) * (256 * (LIT_NT + 1) + 512);
+  return BF_OK;
+}
+
+// One call: validation, launch shape, and (unless dry) the launches.
+bf_status run(const bf_plan* const* plans, int nplans, const void* d_in, float* d_out, int n_frames, int H, int W,
+              cudaStream_t st, const bf_apply_args* args, bf_launch_config* dry, bool dump = false) {
+  bf_apply_args A;
+  bf_apply_args_default(&A);
+  if (args) A = *args;
+  if (!plans || nplans < 1 || nplans > MAXP || H <= 0 || W <= 0 || n_frames <= 0) return BF_ERR_INVALID_ARG;
+  for (int q = 0; q < nplans; ++q)
+    if (!plans[q]) return BF_ERR_INVALID_ARG;
+  if (!dry && (!d_in || !d_out)) return BF_ERR_INVALID_ARG;
+  if ((long long)H * W > (1LL << 40) / n_frames) return BF_ERR_INVALID_ARG;
+  if (!dry && !dump && (const void*)d_out == d_in) return BF_ERR_INVALID_ARG;
+  int ya = A.row_begin, yb = A.row_end;
+  if (ya == 0 && yb == 0) yb = H;
+  if (ya < 0 || ya >= yb || yb > H) return BF_ERR_INVALID_ARG;
+  if (A.band_rows < 0) return BF_ERR_INVALID_ARG;
+  // union of the plans' selected k (one set of channels); a single plan is its own union
+  bf_plan merged = *plans[0];
+  if (nplans > 1) {
+    if (n_frames != 1) return BF_ERR_INVALID_ARG;
+    int ks[BF_MAX_TERMS * MAXP], nks = 0;
+    for (int q = 0; q < nplans; ++q) {
+      if (!same_channels(plans[0], plans[q]) || plans[q]->literal != plans[0]->literal) return BF_ERR_INVALID_ARG;
+      for (int i = 0; i < plans[q]->n_k; ++i) ks[nks++] = plans[q]->k[i];
+    }
+    std::sort(ks, ks + nks);
+    nks = (int)(std::unique(ks, ks + nks) - ks);
+    if (nks > 16) return BF_ERR_UNSUPPORTED;
+    merged.n_k = nks;
+    for (int i = 0; i < nks; ++i) {
+      merged.k[i] = ks[i];
+      merged.a[i] = 0.0;
+    }
+  }
+  const bf_plan* p = &merged;
+  if (p->literal) {
+    if (nplans != 1 || ya != 0 || yb != H || dump) return BF_ERR_UNSUPPORTED;
+    LParams Lp;
+    dim3 grid;
+    size_t smem;
+    const bf_status s = literal_launch(p, n_frames, H, W, Lp, grid, smem);
+    if (s != BF_OK) return s;
+    if (A.band_rows > 0) {
+      Lp.TH = std::max(1, std::min(H, A.band_rows));
+      grid.y = (H + Lp.TH - 1) / Lp.TH;
+    }
+    if (dry) {
+      *dry = bf_launch_config{1, "bf_literal_kernel", LIT_NT, (int)grid.x, (int)grid.y, n_frames, Lp.TW, Lp.TH,
+                              smem, 1, p->n_k, 1, 0};
+      return BF_OK;
+    }
+    Lp.fb_count = A.d_fallback_count;
+    Lp.fb_mask = A.d_fallback_mask;
+    return launch_literal(Lp, static_cast<const unsigned char*>(d_in), d_out, grid, smem, st) == cudaSuccess
+               ? BF_OK
+               : BF_ERR_CUDA;
+  }
+  if (A.u8_trig != 0 && A.u8_trig != 1) return BF_ERR_INVALID_ARG;
+  Req R{plans, nplans, n_frames, H, W, ya, yb, A.kernel, A.band_rows, dump, A.u8_trig == 1};
+  Launch L;
+  const bf_status s = prepare(R, p, L);
+  if (s != BF_OK) return s;
+  if (dry) {
+    *dry = bf_launch_config{L.passes, L.name, L.threads, (int)L.grid.x, (int)L.grid.y, (int)L.grid.z, L.P.TW,
+                            L.P.TH, L.smem, L.P.G, L.spec.kern == KERN_WS2 ? L.P.tpc : L.spec.MAXK, L.spec.COLS,
+                            L.ws_bytes};
+    return BF_OK;
+  }
+  longlong2* ws = nullptr;
+  if (L.ws_bytes > 0) {
+    if (!A.d_workspace || A.workspace_bytes < L.ws_bytes) return BF_ERR_WORKSPACE;
+    ws = static_cast<longlong2*>(A.d_workspace);
+  }
+  const int wbits = dump ? 0 : combine_bits(plans, nplans);
+  L.P.fb_count = A.d_fallback_count;
+  L.P.fb_mask = A.d_fallback_mask;
+  if (!dump) {
+    const bf_status rs = repair_sink(A, std::ldexp(1.0, wbits), mass_full(p, L.P), st, L.P.rep);
+    if (rs != BF_OK) return rs;
+  }
+  cudaError_t err = cudaSuccess;
+  if (L.spec.kern == KERN_WS2 && !dump) {   // one launch, every term (split over the cluster)
+    set_terms(R, p, 0, p->n_k, wbits, L.P);
+    L.P.pass = 0;
+    err = dispatch(L.spec, L.P, d_in, d_out, ws, L.grid, L.smem, st);
+  } else {
+    const int per = dump ? 16 : L.spec.MAXK;
+    for (int pass = 0; pass < L.passes && err == cudaSuccess; ++pass) {
+      const int first = pass * per;
+      const int nk = std::min(per, p->n_k - first);
+      set_terms(R, p, first, nk, wbits, L.P);
+      L.P.ngrp = (4 * nk + 31) / 32;
+      LaunchSpec sp = L.spec;
+      sp.FULL = (nk == sp.MAXK);
+      if (sp.NPL > 1) sp.FULL = false;
+      for (int i = 1; i < nk; ++i)
+        if (L.P.kval[i] != L.P.kval[i - 1] + 1) sp.CONSEC = false;
+      if (dump) {
+        L.P.pass = 0;
+      } else {
+        L.P.pass = (L.passes == 1) ? 0 : (pass == 0 ? 1 : (pass == L.passes - 1 ? 3 : 2));
+        // walker segments (kernel 1): ngrp * nseg warps; long segments amortise the window sums
+        if (sp.kern == KERN_BAND) {
+          const int max_tasks = sp.NT / 32;
+          const int halo = L.P.TW >= 0 ? (sp.NT - L.P.TW) : 0;
+          int nseg = std::max(1, max_tasks / L.P.ngrp);
+          const int min_len = std::max(32, 2 * (halo + 1) / 3);
+          while (nseg > 1 && (L.P.TW + nseg - 1) / nseg < min_len) --nseg;
+          // wide halos (NT = 512): four segments measured best on cfg4 (r = 192)
+          if (sp.NT == 512) nseg = std::min(4, std::max(1, max_tasks / L.P.ngrp));
+          L.P.nseg = nseg;
+          L.P.seglen = (L.P.TW + nseg - 1) / nseg;
+          L.P.seglen += L.P.seglen & 1;
+        } else if (sp.kern == KERN_WS) {   // F warps: (WS_F / 32) / ngrp segments per group
+          L.P.nseg = std::max(1, (WS_F / 32) / L.P.ngrp);
+          L.P.seglen = (L.P.TW + L.P.nseg - 1) / L.P.nseg;
+          L.P.seglen += L.P.seglen & 1;
+        }
+      }
+      err = dispatch(sp, L.P, d_in, d_out, ws, L.grid, L.smem, st);
+    }
+  }
+  if (err == cudaSuccess && L.P.rep.count) {
+    RParams Rp;
+    repair_params(plans, nplans, n_frames, H, W, A, L.P.rep, Rp);
+    err = launch_repair(Rp, d_in, d_out, st);
+  }
+  return err == cudaSuccess ? BF_OK : BF_ERR_CUDA;
+}
+
+// ---- Case 1 cache: fingerprint of everything the cached channels depend on
+unsigned long long spatial_key(const bf_plan* p) {
+  KParams P;
+  std::memset(&P, 0, sizeof(P));
+  quantise(p, P);
+  unsigned long long h = 1469598103934665603ULL;
+  auto mix = [&](const void* d, size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(d);
+    for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ULL;
+  };
+  mix(&P.ns, sizeof(int));
+  mix(&P.nby, sizeof(int));
+  mix(P.vlo, sizeof(P.vlo));
+  mix(P.vhi, sizeof(P.vhi));
+  mix(P.qs, sizeof(P.qs));
+  mix(P.qsD, sizeof(P.qsD));
+  mix(&P.ush, sizeof(int));
+  mix(P.nbx, sizeof(P.nbx));
+  mix(P.hlo, sizeof(P.hlo));
+  mix(P.hhi, sizeof(P.hhi));
+  mix(P.ax, sizeof(P.ax));
+  mix(&P.D, sizeof(double));
+  mix(&p->input_dtype, sizeof(int));
+  return h;
+}
+
+// ---- bf_apply_host: device buffers, streams and events per device
+constexpr int HOST_CHUNKS = 5;
+struct HostCache {
+  std::mutex mu;
+  bool ready = false;
+  void* din = nullptr;
+  float* dout = nullptr;
+  void* dws = nullptr;
+  size_t in_bytes = 0, out_bytes = 0, ws_bytes = 0;
+  cudaStream_t s_in = nullptr, s_k = nullptr, s_k2 = nullptr, s_out = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_in[HOST_CHUNKS] = {}, ev_k[HOST_CHUNKS] = {};
+  cudaError_t setup() {
+    if (ready) return cudaSuccess;
+    cudaError_t e = cudaSuccess;
+    for (cudaStream_t* q : {&s_in, &s_k, &s_k2, &s_out})
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(q, cudaStreamNonBlocking);
+    for (cudaEvent_t* v : {&ev_start, &ev_end})
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(v, cudaEventDisableTiming);
+    for (int j = 0; j < HOST_CHUNKS && e == cudaSuccess; ++j) {
+      e = cudaEventCreateWithFlags(&ev_in[j], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_k[j], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) ready = true;
+    return e;
+  }
+  // grows *buf to at least `need` bytes (the size is reset before the allocation, so a failure
+  // leaves an empty buffer, never a stale size)
+  static cudaError_t grow(void** buf, size_t* have, size_t need) {
+    if (*have >= need) return cudaSuccess;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *have = 0;
+    const cudaError_t e = cudaMalloc(buf, need);
+    if (e == cudaSuccess) *have = need;
+    return e;
+  }
+};
+HostCache g_host[MAX_DEV];
+
+}  // namespace
+
+extern "C" void bf_apply_args_default(bf_apply_args* a) {
+  if (a) std::memset(a, 0, sizeof(*a));
+}
+
+extern "C" bf_status bf_apply_launches(const bf_plan* p, int H, int W, int* n) {
+  if (!p || !n || H <= 0 || W <= 0) return BF_ERR_INVALID_ARG;
+  *n = 0;
+  bf_launch_config c;
+  const bf_status s = run(&p, 1, nullptr, nullptr, 1, H, W, nullptr, nullptr, &c);
+  if (s == BF_OK) *n = c.n_launches;
+  return s;
+}
+
+extern "C" bf_status bf_apply_config(const bf_plan* plan, int n_frames, int H, int W, const bf_apply_args* args,
+                                     bf_launch_config* cfg) {
+  if (!plan || !cfg || H <= 0 || W <= 0 || n_frames <= 0) return BF_ERR_INVALID_ARG;
+  return run(&plan, 1, nullptr, nullptr, n_frames, H, W, nullptr, args, cfg);
+}
+
+extern "C" bf_status bf_workspace_size(const bf_plan* plan, int n_frames, int H, int W, const bf_apply_args* args,
+                                       size_t* bytes) {
+  if (!bytes) return BF_ERR_INVALID_ARG;
+  *bytes = 0;
+  bf_launch_config c;
+  const bf_status s = bf_apply_config(plan, n_frames, H, W, args, &c);
+  if (s == BF_OK) *bytes = c.workspace_bytes;
+  return s;
+}
+
+extern "C" bf_status bf_apply(const bf_plan* plan, const void* d_in, float* d_out, int H, int W, bf_stream stream) {
+  return run(&plan, 1, d_in, d_out, 1, H, W, reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr);
+}
+
+extern "C" bf_status bf_apply_ex(const bf_plan* plan, const void* d_in, float* d_out, int n_frames, int H, int W,
+                                 bf_stream stream, const bf_apply_args* args) {
+  return run(&plan, 1, d_in, d_out, n_frames, H, W, reinterpret_cast<cudaStream_t>(stream), args, nullptr);
+}
+
+extern "C" bf_status bf_apply_multi(const bf_plan* const* plans, int n_plans, const void* d_in, float* d_out, int H,
+                                    int W, bf_stream stream) {
+  return run(plans, n_plans, d_in, d_out, 1, H, W, reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr);
+}
+
+extern "C" bf_status bf_apply_batched(const bf_plan* plan, const void* d_in, float* d_out, int n_frames, int H,
+                                      int W, bf_stream stream) {
+  return run(&plan, 1, d_in, d_out, n_frames, H, W, reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr);
+}
+
+extern "C" bf_status bf_cache_size(const bf_plan* plan, int k_count, int H, int W, size_t* bytes) {
+  if (!plan || !bytes || H <= 0 || W <= 0 || k_count < 1 || k_count > BF_MAX_TERMS) return BF_ERR_INVALID_ARG;
+  *bytes = sizeof(int) * 4 * (size_t)k_count * H * W;
+  return BF_OK;
+}
+
+extern "C" bf_status bf_precompute(const bf_plan* plan, int k_count, const void* d_in, int H, int W, void* d_cache,
+                                   size_t cache_bytes, bf_stream stream, bf_cache_desc* desc) {
+  size_t need = 0;
+  bf_status s = bf_cache_size(plan, k_count, H, W, &need);
+  if (s != BF_OK) return s;
+  if (!d_in || !d_cache || !desc || cache_bytes < need) return BF_ERR_INVALID_ARG;
+  if (plan->literal) return BF_ERR_UNSUPPORTED;
+  int rlo, rhi;
+  const int form = plan_form(plan, rlo, rhi);
+  if (form != 1 && form != 2) return BF_ERR_UNSUPPORTED;
+  bf_plan q = *plan;   // channels of k = 0 .. k_count - 1
+  q.n_k = k_count;
+  for (int i = 0; i < k_count; ++i) {
+    q.k[i] = i;
+    q.a[i] = 0.0;
+  }
+  const bf_plan* qp = &q;
+  // the launch parameters point at the cache: reuse run() with the dump flag
+  Req R{&qp, 1, 1, H, W, 0, H, BF_KERNEL_AUTO, 0, true, false};
+  Launch L;
+  s = prepare(R, qp, L);
+  if (s != BF_OK) return s;
+  L.P.cache = static_cast<int*>(d_cache);
+  L.P.cache_plane = (long long)H * W;
+  cudaError_t err = cudaSuccess;
+  for (int pass = 0; pass < L.passes && err == cudaSuccess; ++pass) {
+    const int first = pass * 16, nk = std::min(16, k_count - first);
+    set_terms(R, qp, first, nk, 0, L.P);
+    L.P.ngrp = (4 * nk + 31) / 32;
+    L.P.pass = 0;
+    LaunchSpec sp = L.spec;
+    sp.FULL = nk == 16;
+    err = dispatch(sp, L.P, d_in, nullptr, nullptr, L.grid, L.smem, reinterpret_cast<cudaStream_t>(stream));
+  }
+  if (err != cudaSuccess) return BF_ERR_CUDA;
+  desc->k_count = k_count;
+  desc->H = H;
+  desc->W = W;
+  desc->input_dtype = plan->input_dtype;
+  desc->intensity_max = plan->D;
+  desc->spatial_key = spatial_key(plan);
+  return BF_OK;
+}
+
+extern "C" bf_status bf_apply_cached(const bf_plan* plan, const bf_cache_desc* desc, const void* d_cache,
+                                     const void* d_in, float* d_out, bf_stream stream, const bf_apply_args* args) {
+  if (!plan || !desc || !d_cache || !d_in || !d_out || (const void*)d_out == d_in) return BF_ERR_INVALID_ARG;
+  if (plan->literal) return BF_ERR_UNSUPPORTED;
+  if (desc->H <= 0 || desc->W <= 0 || plan->input_dtype != desc->input_dtype || plan->D != desc->intensity_max ||
+      spatial_key(plan) != desc->spatial_key)
+    return BF_ERR_INVALID_ARG;
+  for (int i = 0; i < plan->n_k; ++i)
+    if (plan->k[i] >= desc->k_count) return BF_ERR_INVALID_ARG;
+  bf_apply_args A;
+  bf_apply_args_default(&A);
+  if (args) A = *args;
+  CParams C;
+  std::memset(&C, 0, sizeof(C));
+  C.H = desc->H;
+  C.W = desc->W;
+  C.plane = (long long)desc->H * desc->W;
+  C.nk = plan->n_k;
+  const int wbits = combine_bits(&plan, 1);
+  for (int i = 0; i < plan->n_k; ++i) {
+    C.ch[i] = plan->k[i];
+    C.kval[i] = plan->k[i];
+    C.aw[i] = std::ldexp(plan->a[i], wbits);
+  }
+  C.invD = 1.0 / plan->D;
+  C.D = plan->D;
+  C.u8 = plan->input_dtype == BF_IN_U8;
+  C.fb_count = A.d_fallback_count;
+  C.fb_mask = A.d_fallback_mask;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  KParams Q;
+  std::memset(&Q, 0, sizeof(Q));
+  quantise(plan, Q);
+  const bf_status rs = repair_sink(A, std::ldexp(1.0, wbits), mass_full(plan, Q), st, C.rep);
+  if (rs != BF_OK) return rs;
+  cudaError_t err = launch_cached(C, static_cast<const int*>(d_cache), d_in, d_out, st);
+  if (err == cudaSuccess && C.rep.count) {
+    RParams Rp;
+    repair_params(&plan, 1, 1, desc->H, desc->W, A, C.rep, Rp);
+    err = launch_repair(Rp, d_in, d_out, st);
+  }
+  return err == cudaSuccess ? BF_OK : BF_ERR_CUDA;
+}
+
+extern "C" bf_status bf_apply_host(const bf_plan* plan, const void* h_in, float* h_out, int H, int W,
+                                   bf_stream stream) {
+  if (!plan || !h_in || !h_out || H <= 0 || W <= 0) return BF_ERR_INVALID_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t n = (size_t)H * W;
+  const size_t isz = plan->input_dtype == BF_IN_U8 ? 1 : 4;
+  const size_t ib = n * isz, ob = n * 4;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAX_DEV) return BF_ERR_CUDA;
+  size_t wsb = 0;
+  bf_status s = bf_workspace_size(plan, 1, H, W, nullptr, &wsb);
+  if (s != BF_OK) return s;
+  HostCache& hc = g_host[dev];
+  std::lock_guard<std::mutex> lk(hc.mu);
+  if (hc.setup() != cudaSuccess) return BF_ERR_CUDA;
+  if (HostCache::grow(&hc.din, &hc.in_bytes, ib) != cudaSuccess) return BF_ERR_CUDA;
+  if (HostCache::grow(reinterpret_cast<void**>(&hc.dout), &hc.out_bytes, ob) != cudaSuccess) return BF_ERR_CUDA;
+  if (wsb && HostCache::grow(&hc.dws, &hc.ws_bytes, wsb) != cudaSuccess) return BF_ERR_CUDA;
+  // Row chunks pipelined over three streams: the copy of input piece j+1, the filter of output
+  // rows [b_j, b_j+1) and the copy back of chunk j-1 overlap. Input piece j holds rows
+  // [b_j + rv, b_j+1 + rv) (piece 0 from row 0, the last to row H), so the filter of chunk j,
+  // which reads rows b_j - rv .. b_j+1 - 1 + rv, needs pieces 0..j only. Small images, the
+  // literal kernel, multi-pass plans and chunks shorter than 512 rows take one chunk.
+  int rv = 0;
+  for (int b = 0; b < plan->snby[0]; ++b) rv = std::max(rv, std::max(-plan->sloy[0][b], plan->shiy[0][b]));
+  int K = (plan->literal || wsb || n < (1u << 20)) ? 1 : std::min(HOST_CHUNKS, 1 + H / std::max(512, 2 * rv + 2));
+  K = std::max(K, 1);
+  // chunk boundaries with weights 1/2, 1, ..., 1, 1/2 (the pipeline's fill and drain are one
+  // input piece and one output chunk); every chunk non-empty
+  auto bnd = [&](int j) {
+    if (j <= 0) return 0;
+    if (j >= K) return H;
+    if (K <= 2) return (int)((long long)H * j / K);
+    return (int)((long long)H * (2 * (j - 1) + 1) / (2 * (K - 2) + 2));
+  };
+  cudaError_t e = cudaEventRecord(hc.ev_start, st);   // ordered after the caller's prior work
+  for (cudaStream_t q : {hc.s_in, hc.s_k, hc.s_k2, hc.s_out})
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(q, hc.ev_start, 0);
+  if (e != cudaSuccess) return BF_ERR_CUDA;
+  const unsigned char* hin = static_cast<const unsigned char*>(h_in);
+  unsigned char* din = static_cast<unsigned char*>(hc.din);
+  for (int j = 0; j < K && e == cudaSuccess; ++j) {
+    const int r0 = j == 0 ? 0 : std::min(H, bnd(j) + rv), r1 = j == K - 1 ? H : std::min(H, bnd(j + 1) + rv);
+    if (r1 > r0)
+      e = cudaMemcpyAsync(din + (size_t)r0 * W * isz, hin + (size_t)r0 * W * isz, (size_t)(r1 - r0) * W * isz,
+                          cudaMemcpyHostToDevice, hc.s_in);
+    if (e == cudaSuccess) e = cudaEventRecord(hc.ev_in[j], hc.s_in);
+  }
+  s = BF_OK;
+  for (int j = 0; j < K && e == cudaSuccess && s == BF_OK; ++j) {
+    // alternate two compute streams: chunk j+1 may start on the SMs chunk j's last CTAs leave
+    cudaStream_t sk = (j & 1) ? hc.s_k2 : hc.s_k;
+    e = cudaStreamWaitEvent(sk, hc.ev_in[j], 0);
+    if (e != cudaSuccess) break;
+    bf_apply_args A;
+    bf_apply_args_default(&A);
+    A.row_begin = bnd(j);
+    A.row_end = bnd(j + 1);
+    A.d_workspace = hc.dws;
+    A.workspace_bytes = hc.ws_bytes;
+    if (K == 1) A.row_begin = A.row_end = 0;
+    s = run(&plan, 1, hc.din, hc.dout, 1, H, W, sk, &A, nullptr);
+    if (s != BF_OK) break;
+    e = cudaEventRecord(hc.ev_k[j], sk);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hc.s_out, hc.ev_k[j], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h_out + (size_t)bnd(j) * W, hc.dout + (size_t)bnd(j) * W,
+                          (size_t)(bnd(j + 1) - bnd(j)) * W * 4, cudaMemcpyDeviceToHost, hc.s_out);
+  }
+  // join: the caller's stream waits for all four, then the call returns with h_out complete
+  for (cudaStream_t q : {hc.s_in, hc.s_k, hc.s_k2, hc.s_out}) {
+    cudaEventRecord(hc.ev_end, q);
+    cudaStreamWaitEvent(st, hc.ev_end, 0);
+  }
+  const cudaError_t es = cudaStreamSynchronize(st);
+  if (s != BF_OK) return s;
+  return (e == cudaSuccess && es == cudaSuccess) ? BF_OK : BF_ERR_CUDA;
+}

@@ -1,0 +1,168 @@
+// fp64 repair of ill-conditioned pixels (reading Q27).
+//
+// The fused kernels flag a pixel when its denominator is small against the clipped spatial
+// mass (cond = den / sum K~_s < tau, or den <= 0): there out = num / den amplifies the integer
+// format's rounding (relative ~1e-8 of the full-window denominator) by 1 / cond, and the
+// fallback decision (den <= 0, Q18) rides on it. This kernel re-evaluates each flagged pixel in
+// fp64 from the approximated kernels themselves, the direct double loop of pin P1
+//     num(x) = sum_y K~_s(x - y) K~_r(I(x) - I(y)) I(y),   den(x) = sum_y K~_s(x - y) K~_r(I(x) - I(y)),
+// K~_r(t) = sum_k a_k cos(pi k t / T) (eq:trigonometric_N_terms), K~_s the lowered
+// boxes (eq:Box_N_terms), which equals the box evaluation eq:numerator_2D_box_N_terms
+// mathematically. One CTA per flagged pixel, a fixed-order block reduction
+// (deterministic); u8 inputs tabulate K~_r on the 511 integer differences.
+#include <algorithm>
+#include <atomic>
+
+#include "bf_device.cuh"
+
+namespace bf {
+
+__device__ unsigned g_rep_count[REPAIR_SLOTS];
+__device__ unsigned long long g_rep_list[REPAIR_SLOTS][REPAIR_CAP];
+
+namespace {
+
+constexpr int RT = 256;
+
+// K~_r(t) for plan q: Chebyshev recurrence cos((k+1) th) = 2 cos th cos(k th) - cos((k-1) th) in fp64
+__device__ __forceinline__ double range_approx(const RParams& R, int q, double t) {
+  double s1, c1;
+  sincospi(t / R.T, &s1, &c1);
+  double cp = c1, c = 1.0, acc = 0.0;   // cos(-th), cos(0)
+  int kk = 0;
+  const int n = R.nkp[q];
+  for (int i = 0; i < n; ++i) {
+    for (; kk < R.k[q][i]; ++kk) {
+      const double cn = fma(2.0 * c1, c, -cp);
+      cp = c;
+      c = cn;
+    }
+    acc = fma(R.a[q][i], c, acc);
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(RT) bf_repair_kernel(const RParams R, const void* __restrict__ in,
+                                                       float* __restrict__ out) {
+  extern __shared__ double sm[];
+  const int n1 = 2 * R.rad + 1;
+  double* fx = sm;              // [2][n1]: fx_s(u), u = -rad..rad
+  double* fy = sm + 2 * n1;     // [2][n1]
+  double* klut = sm + 4 * n1;   // [511] K~_r(t), t = -255..255 (u8)
+  __shared__ double red[2][RT / 32];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 2 * n1; i += RT) {
+    const int s = i / n1, o = i % n1 - R.rad;
+    double wx = 0.0, wy = 0.0;
+    if (s < R.ns) {
+      for (int b = 0; b < R.nbx[s]; ++b)
+        if (o >= R.lox[s][b] && o <= R.hix[s][b]) wx += R.wx[s][b];
+      for (int b = 0; b < R.nby[s]; ++b)
+        if (o >= R.loy[s][b] && o <= R.hiy[s][b]) wy += R.wy[s][b];
+    }
+    fx[i] = wx;
+    fy[i] = wy;
+  }
+  const unsigned n = min(*R.count, R.cap);
+  int lut_q = -1;
+  for (unsigned it = blockIdx.x; it < n; it += gridDim.x) {
+    const unsigned long long e = R.list[it];
+    const int q = R.nplans > 1 ? (int)(e / (unsigned long long)R.plan_stride) : 0;
+    const long long pix = (long long)(e - (unsigned long long)q * (unsigned long long)R.plan_stride);
+    const long long f = pix / R.frame_elems;
+    const long long rem = pix - f * R.frame_elems;
+    const int y = (int)(rem / R.W), x = (int)(rem % R.W);
+    const long long fbase = f * R.frame_elems;
+    __syncthreads();   // (previous pixel's table / reduction done)
+    if (R.u8 && lut_q != q) {
+      for (int t = tid; t < 511; t += RT) klut[t] = range_approx(R, q, (double)(t - 255));
+      lut_q = q;
+    }
+    __syncthreads();
+    const double Ix = R.u8 ? (double)reinterpret_cast<const unsigned char*>(in)[pix]
+                           : (double)reinterpret_cast<const float*>(in)[pix];
+    const int ya = max(0, y - R.rad), yb = min(R.H - 1, y + R.rad);
+    const int xa = max(0, x - R.rad), xb = min(R.W - 1, x + R.rad);
+    const int nc = xb - xa + 1;
+    const long long ntap = (long long)(yb - ya + 1) * nc;
+    double num = 0.0, den = 0.0;
+    for (long long i = tid; i < ntap; i += RT) {
+      const int row = ya + (int)(i / nc), col = xa + (int)(i % nc);
+      const int v = row - y + R.rad, u = col - x + R.rad;
+      double ks = fx[u] * fy[v];
+      if (R.ns > 1) ks = fma(fx[n1 + u], fy[n1 + v], ks);
+      if (ks == 0.0) continue;
+      const long long idx = fbase + (long long)row * R.W + col;
+      double Iy, kr;
+      if (R.u8) {
+        const int iy = reinterpret_cast<const unsigned char*>(in)[idx];
+        Iy = (double)iy;
+        kr = klut[(int)Ix - iy + 255];
+      } else {
+        Iy = (double)__ldg(reinterpret_cast<const float*>(in) + idx);
+        kr = range_approx(R, q, Ix - Iy);
+      }
+      const double w = ks * kr;
+      den += w;
+      num = fma(w, Iy, num);
+    }
+    // fixed-order block reduction
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      num += __shfl_xor_sync(0xffffffffu, num, o);
+      den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    if ((tid & 31) == 0) {
+      red[0][tid >> 5] = num;
+      red[1][tid >> 5] = den;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double sn = 0.0, sd = 0.0;
+      for (int w = 0; w < RT / 32; ++w) {
+        sn += red[0][w];
+        sd += red[1][w];
+      }
+      const bool fb = !(sd > 0.0);
+      out[e] = fb ? (float)Ix : (float)(sn / sd);
+      if (R.fb_mask) R.fb_mask[e] = fb ? 1 : 0;
+      if (fb && R.fb_count) atomicAdd(R.fb_count, 1ULL);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t repair_slot(unsigned s, unsigned** count, unsigned long long** list) {
+  // symbol addresses per device, looked up once (no runtime query inside a stream capture later)
+  static std::atomic<void*> cache_c[64], cache_l[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  void* c = dev < 64 ? cache_c[dev].load() : nullptr;
+  void* l = dev < 64 ? cache_l[dev].load() : nullptr;
+  if (!c || !l) {
+    e = cudaGetSymbolAddress(&c, g_rep_count);
+    if (e == cudaSuccess) e = cudaGetSymbolAddress(&l, g_rep_list);
+    if (e != cudaSuccess) return e;
+    if (dev < 64) {
+      cache_c[dev].store(c);
+      cache_l[dev].store(l);
+    }
+  }
+  *count = static_cast<unsigned*>(c) + s;
+  *list = static_cast<unsigned long long*>(l) + (size_t)s * REPAIR_CAP;
+  return cudaSuccess;
+}
+
+cudaError_t launch_repair(const RParams& R, const void* in, float* out, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (4 * (2 * (size_t)R.rad + 1) + 512);
+  cudaError_t e = cudaFuncSetAttribute(bf_repair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  bf_repair_kernel<<<4 * std::max(1, nsm), RT, smem, st>>>(R, in, out);
+  return cudaGetLastError();
+}
+
+}  // namespace bf

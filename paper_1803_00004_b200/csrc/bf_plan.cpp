@@ -521,8 +521,9 @@ extern "C" const char* bf_status_string(bf_status s) {
     case BF_ERR_NO_MEMORY: return "BF_ERR_NO_MEMORY: host allocation failed";
     case BF_ERR_CUDA: return "BF_ERR_CUDA: CUDA launch or runtime error";
     case BF_ERR_NUMERIC: return "BF_ERR_NUMERIC: the fit produced no usable term";
+    case BF_ERR_WORKSPACE: return "BF_ERR_WORKSPACE: the plan runs in several passes and needs a device workspace";
   }
   return "unknown bf_status";
 }
 
-extern "C" const char* bf_version(void) { return "bf-b200 0.1.0"; }
+extern "C" const char* bf_version(void) { return "bf-b200 0.2.0"; }

@@ -1,0 +1,356 @@
+// Kernel 2b: fused box differences + combine (bf_ws2_kernel), the default T = D kernel for
+// separable plans with at most two boxes per axis. Three warp-specialised roles joined by a
+// two-deep ring of U' rows and named barriers (bar.arrive / bar.sync per row parity and
+// 32-channel group):
+//   FH  warps 0..      one thread per output pixel: for every channel slot of group g,
+//                      F = round(sum_b (Q[x + hi_b + 1] - Q[x + lo_b]) ax_b / 2^32) (lanes = consecutive
+//                      x: conflict-free), accumulated straight into the exact int64 num / den with
+//                      the pixel's fp64 combine weights (per range plan for bf_apply_multi)
+//   S   next warps     warp g turns group g's U' rows into exclusive prefix rows Q in place
+//   V   last 12 warps  COLS extended columns per thread: slides the vertical sums, writes U'(y)
+// FH has the lowest warp ids (the schedulers favour older warps; FH is the critical role).
+//
+// COLS = 2 (wide radii, e.g. cfg4's r = 192): each V thread keeps the vertical state of two
+// columns 384 apart, so a strip covers 768 extended columns (output strip 352 wide instead of
+// 0 at a 384-column halo) with 8 terms per CTA.
+//
+// CL: the range terms are split over a cluster of G CTAs on the same strip and band (CTA c owns
+// terms [c tpc, c tpc + tpc)): every CTA computes its partial int64 num / den per output pixel;
+// CTAs 1..G-1 send them to CTA 0 with st.async into CTA 0's shared memory (distributed shared
+// memory), completing CTA 0's per-row-parity mbarrier FULL[b] by transaction bytes; CTA 0 adds
+// them (exact integers: the result is bitwise that of one CTA doing all terms) and releases the
+// slot through the senders' EMPTY[b] mbarriers. No HBM workspace and one launch for up to
+// G * tpc terms (cfg4: 24 terms = 3 CTAs x 8).
+//
+// DUMP (bf_precompute, Case 1 of P:1200-1219): FH writes the box-filtered channels F of its pixel
+// to the cache planes instead of combining them.
+#pragma once
+
+#include "bf_device.cuh"
+
+namespace bf {
+namespace ws2 {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned map_rank(unsigned laddr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(laddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(unsigned a, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned a, unsigned bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1;\n}" ::"r"(a),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(unsigned raddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
+}
+__device__ __forceinline__ void st_async_pair(unsigned raddr, long long a, long long b, unsigned rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.s64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "l"(a), "l"(b), "r"(rmbar)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+constexpr int MBAR_BYTES = 64;   // mbarriers at the start of shared memory (FULL[2], EMPTY[2])
+
+template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL, int NPL, int COLS, bool CL, bool DUMP>
+__global__ void __launch_bounds__(W2_THREADS, 1)
+    bf_ws2_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out, longlong2* __restrict__ ws) {
+  constexpr int NS = Form<FORM>::NS, NB = Form<FORM>::NBY, NBX = Form<FORM>::NBX;
+  constexpr int M = NS * NBX;
+  static_assert(NS == 1 && M <= 2, "the FH role handles separable forms with at most two x boxes");
+  static_assert(COLS == 1 || MAXK == 8, "two columns per V thread: 8 terms per CTA (one channel group)");
+  constexpr int NFH = w2_nfh(COLS), NSW = w2_ns(COLS);
+  constexpr int H0 = 0, S0 = NFH, V0 = NFH + NSW;
+  static_assert(V0 + W2_V == W2_THREADS, "role sizes");
+  constexpr int UP = w2_up(COLS);
+  constexpr int VREG = NPL > 1 ? 104 : 112, OREG = NPL > 1 ? 56 : 48;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem_raw);   // FULL[2], EMPTY[2]
+  int* Ubuf = reinterpret_cast<int*>(smem_raw + MBAR_BYTES);                     // [2][4 nk][UP]
+  float2* lut = reinterpret_cast<float2*>(smem_raw + P.l_off);
+  double2* lut64 = reinterpret_cast<double2*>(lut + 256);
+  longlong2* red = reinterpret_cast<longlong2*>(smem_raw + P.r_off);              // [2][G-1][TW]
+
+  const int tid = threadIdx.x;
+  const int G = CL ? P.G : 1;
+  const int rank = CL ? (int)cluster_rank() : 0;
+  const int t0 = CL ? rank * P.tpc : 0;                      // this CTA's terms [t0, t0 + nkc)
+  const int nkc = CL ? min(P.tpc, P.nk - t0) : P.nk;
+  const int ngrp = (4 * nkc + 31) >> 5;
+  const int x0 = (CL ? (int)blockIdx.x / G : (int)blockIdx.x) * P.TW;
+  const int y0 = P.yb + blockIdx.y * P.TH;
+  const long long fbase = (long long)blockIdx.z * P.frame_elems;
+  const int TWv = min(P.TW, P.W - x0);
+  const int yend = min(y0 + P.TH, P.ye);
+  const int wv = P.wv;                            // extended columns scanned (multiple of 8, <= W2_V * COLS)
+  const int srow = 4 * nkc * UP;                  // ints per U' buffer
+  constexpr int n_ufull = W2_V + 32;              // U_FULL: V arrive, S_g sync
+  constexpr int n_uempty = W2_V + NFH;            // U_EMPTY: FH arrive, V sync
+  constexpr int n_qfull = 32 + NFH;               // Q_FULL: S_g arrive, FH sync
+
+  fill_luts<U8>(P, lut, lut64, tid, W2_THREADS);
+  if constexpr (CL) {
+    if (tid == 0) {
+      mbar_init(smem_u32(&mbar[0]), 1);           // FULL[b]: CTA 0's expect_tx arrival + the senders' bytes
+      mbar_init(smem_u32(&mbar[1]), 1);
+      mbar_init(smem_u32(&mbar[2]), NFH / 32);    // EMPTY[b]: every FH warp of CTA 0 once per row
+      mbar_init(smem_u32(&mbar[3]), NFH / 32);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster_sync();
+  } else {
+    __syncthreads();
+  }
+
+  if (tid >= V0) {
+    // ------------------------------------------------------------ V role
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(VREG));
+    const int vt = tid - V0;
+    int col[COLS];
+    bool colok[COLS], vwork[COLS];
+#pragma unroll
+    for (int j = 0; j < COLS; ++j) {
+      const int e = vt + j * W2_V;                  // extended column
+      col[j] = x0 - P.rlo_x + e;
+      colok[j] = (col[j] >= 0) & (col[j] < P.W) & (e < wv);
+      vwork[j] = ((vt & ~31) + j * W2_V) < wv;     // warp-uniform: this block of 32 columns is scanned
+    }
+    int U[COLS][NS * 4 * MAXK];
+    float Ipre[COLS][NB][2];
+#pragma unroll
+    for (int j = 0; j < COLS; ++j) {
+      if (vwork[j]) {
+        v_init<MAXK, NB, NS, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, U[j]);
+        load_taps<NB, U8>(P, in, fbase, col[j], colok[j], y0, Ipre[j]);
+      }
+    }
+    for (int y = y0; y < yend; ++y) {
+      const int b = (y - y0) & 1;
+      const GroupSync hook{b, n_uempty, n_ufull, y - y0 >= 2};
+      int* Ub = Ubuf + b * srow + vt;
+      if constexpr (COLS == 1) {
+        if (vwork[0]) {
+          float Icur[NB][2];
+#pragma unroll
+          for (int bb = 0; bb < NB; ++bb) {
+            Icur[bb][0] = Ipre[0][bb][0];
+            Icur[bb][1] = Ipre[0][bb][1];
+          }
+          if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col[0], colok[0], y + 1, Ipre[0]);
+          v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP, GroupSync, CL>(P, lut, colok[0], y, t0, nkc, Icur, U[0], Ub, &hook);
+        } else {
+          for (int g = 0; g < ngrp; ++g) {
+            hook.begin(g);
+            hook.end(g);
+          }
+        }
+      } else {
+        hook.begin(0);
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) {
+          if (vwork[j]) {
+            float Icur[NB][2];
+#pragma unroll
+            for (int bb = 0; bb < NB; ++bb) {
+              Icur[bb][0] = Ipre[j][bb][0];
+              Icur[bb][1] = Ipre[j][bb][1];
+            }
+            if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col[j], colok[j], y + 1, Ipre[j]);
+            v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP, GroupSync, CL>(P, lut, colok[j], y, t0, nkc, Icur, U[j],
+                                                                    Ub + j * W2_V);
+          }
+        }
+        hook.end(0);
+      }
+    }
+    // drain: the FH warps' last releases
+    for (int y = max(y0, yend - 2); y < yend; ++y)
+      for (int g = 0; g < ngrp; ++g) bar_sync(BAR_U_EMPTY + 2 * ((y - y0) & 1) + g, n_uempty);
+  } else if (tid >= S0) {
+    // ------------------------------------------------------------ S role: prefix scans
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(OREG));
+    const int g = (tid - S0) >> 5;
+    if (g < ngrp) {
+      const int slot = 32 * g + (tid & 31);
+      const bool act = slot < 4 * nkc;
+      for (int y = y0; y < yend; ++y) {
+        const int b = (y - y0) & 1;
+        bar_sync(BAR_U_FULL + 2 * b + g, n_ufull);
+        if (act) prefix_row(Ubuf + b * srow + slot * UP, wv);
+        bar_arrive(BAR_Q_FULL + 2 * b + g, n_qfull);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ FH role
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(OREG));
+    const int o = tid - H0;
+    const bool act = o < TWv;
+    const bool wact = (o & ~31) < TWv;             // warp has pixels of the strip
+    const int oc = act ? o : 0;
+    // Q offsets (extended index o + rlo) of the x boxes: F = round(sum_b (Q[e_b] - Q[l_b]) ax_b / 2^32)
+    const bool two = (M == 2) && P.nbx[0] == 2;
+    const int e0 = oc + P.rlo_x + P.hhi[0][0] + 1, l0 = oc + P.rlo_x + P.hlo[0][0];
+    const int e1 = two ? oc + P.rlo_x + P.hhi[0][1] + 1 : e0, l1 = two ? oc + P.rlo_x + P.hlo[0][1] : l0;
+    const int ax0 = P.ax[0][0], ax1 = two ? P.ax[0][1] : 0;
+    const long long prow = fbase + x0 + oc;
+    const int k0 = P.kval[t0];
+    // cluster reduction addresses (CL)
+    unsigned full_l = 0, red_l = 0;
+    if constexpr (CL) {
+      full_l = smem_u32(&mbar[0]);
+      red_l = smem_u32(red);
+    }
+    float Inext = act ? load_pixel(in, U8, prow + (long long)y0 * P.W) : 0.f;
+    for (int y = y0; y < yend; ++y) {
+      const int b = (y - y0) & 1;
+      const float Ic = Inext;
+      if (act && y + 1 < yend) Inext = load_pixel(in, U8, prow + (long long)(y + 1) * P.W);
+      long long num[NPL] = {}, den[NPL] = {};
+      int mass = 0;   // F of the k = 0 cosine channel (the clipped spatial mass) for the repair flag
+      if (wact) {
+        double c1, s1;
+        pixel_angle<U8>(P, lut64, Ic, c1, s1);
+        Cheb64 gk;
+        gk.init(c1, s1);
+        for (int j = 0; j < k0; ++j) gk.step();
+        const int* Qb = Ubuf + b * srow;
+#pragma unroll
+        for (int i = 0; i < MAXK; ++i) {
+          if (FULL || i < nkc) {
+            if ((i & 7) == 0) bar_sync(BAR_Q_FULL + 2 * b + (i >> 3), n_qfull);
+            if (!DUMP && i > 0) {   // k_i - k_{i-1} >= 1 steps
+              gk.step();
+              if (!CONSEC)
+                for (int j = 1; j < P.kstep[t0 + i]; ++j) gk.step();
+            }
+            int F[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int* q = Qb + (4 * i + c) * UP;
+              long long f = mad_wide(q[e0] - q[l0], ax0, FRND);
+              if (M == 2) f = mad_wide(q[e1] - q[l1], ax1, f);
+              F[c] = fhi(f);
+            }
+            if (P.kval[t0 + i] == 0) mass = F[0];
+            if constexpr (DUMP) {
+              if (act) {
+                int* cp = P.cache + (long long)(4 * P.kval[t0 + i]) * P.cache_plane + (long long)y * P.W + x0 + o;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) cp[c * P.cache_plane] = F[c];
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < NPL; ++q) {   // Case 1 (bf_apply_multi): every plan over the same F
+                const int wc = __double2loint(fma(gk.c, P.aw[q][t0 + i], MAGIC64));
+                const int wsn = __double2loint(fma(gk.s, P.aw[q][t0 + i], MAGIC64));
+                den[q] = mad_wide(wc, F[0], den[q]);
+                den[q] = mad_wide(wsn, F[1], den[q]);
+                num[q] = mad_wide(wc, F[2], num[q]);
+                num[q] = mad_wide(wsn, F[3], num[q]);
+              }
+            }
+            if ((i & 7) == 7 || (FULL ? i + 1 == MAXK : i + 1 == nkc))
+              bar_arrive(BAR_U_EMPTY + 2 * b + (i >> 3), n_uempty);
+          }
+        }
+      } else {   // warp wholly past the strip: only the barriers
+        for (int g = 0; g < ngrp; ++g) {
+          bar_sync(BAR_Q_FULL + 2 * b + g, n_qfull);
+          bar_arrive(BAR_U_EMPTY + 2 * b + g, n_uempty);
+        }
+      }
+      if constexpr (DUMP) continue;
+      if constexpr (CL) {
+        const unsigned ph = ((y - y0) >> 1) & 1;
+        if (rank > 0) {
+          // sender: wait until CTA 0 has consumed row y - 2 from slot b, then store the partials
+          if (wact) {
+            if (y - y0 >= 2) mbar_wait(smem_u32(&mbar[2 + b]), ph ^ 1);
+            if (act) {
+              const unsigned dst = map_rank(red_l + (unsigned)(((b * (G - 1) + rank - 1) * P.TW + o) * 16), 0);
+              st_async_pair(dst, num[0], den[0], map_rank(full_l + 8 * b, 0));
+            }
+          }
+        } else {
+          if (o == 0) mbar_expect(full_l + 8 * b, (unsigned)((G - 1) * TWv * 16));
+          if (wact) {
+            mbar_wait(full_l + 8 * b, ph);
+            if (act) {
+#pragma unroll 1
+              for (int s = 0; s < G - 1; ++s) {
+                const longlong2 v = red[(b * (G - 1) + s) * P.TW + o];
+                num[0] += v.x;
+                den[0] += v.y;
+              }
+              finish_pixel(P, num[0], den[0], Ic, prow + (long long)y * P.W, out, ws, true, mass);
+            }
+          }
+          __syncwarp();
+          if ((tid & 31) == 0)
+            for (int s = 1; s < G; ++s) mbar_arrive_remote(map_rank(smem_u32(&mbar[2 + b]), s));
+        }
+      } else {
+        if (act) {
+#pragma unroll
+          for (int q = 0; q < NPL; ++q)
+            finish_pixel(P, num[q], den[q], Ic, prow + (long long)y * P.W + q * P.plan_stride, out, ws, q == 0, mass);
+        }
+      }
+    }
+  }
+  if constexpr (CL) {
+    // no CTA may leave while its shared memory can still be the target of a remote operation
+    __syncwarp();
+    cluster_sync();
+  }
+}
+
+template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL, int NPL, int COLS, bool CL, bool DUMP>
+cudaError_t go(const KParams& P, const void* in, float* out, longlong2* ws, dim3 grid, size_t smem, cudaStream_t st) {
+  auto kfn = bf_ws2_kernel<MAXK, FORM, U8, CONSEC, FULL, NPL, COLS, CL, DUMP>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if constexpr (CL) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(W2_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P.G;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kfn, P, in, out, ws);
+    if (e != cudaSuccess) return e;
+  } else {
+    kfn<<<grid, W2_THREADS, smem, st>>>(P, in, out, ws);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ws2
+}  // namespace bf

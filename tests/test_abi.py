@@ -29,8 +29,10 @@ def header_functions():
 
 def test_header_declares_expected_api():
     assert header_functions() == sorted(["bf_plan_options_default", "bf_plan_create", "bf_plan_destroy",
-                                         "bf_plan_get_info", "bf_apply", "bf_apply_batched", "bf_apply_host",
+                                         "bf_plan_get_info", "bf_apply", "bf_apply_args_default", "bf_apply_ex",
+                                         "bf_workspace_size", "bf_apply_batched", "bf_apply_host",
                                          "bf_apply_config", "bf_apply_launches", "bf_apply_multi",
+                                         "bf_cache_size", "bf_precompute", "bf_apply_cached",
                                          "bf_status_string", "bf_version"])
 
 
@@ -46,7 +48,7 @@ def test_library_exports_every_declared_symbol(bfmod):
 
 def test_status_strings_and_version(bfmod):
     L = bfmod.lib()
-    for s in range(6):
+    for s in range(7):
         assert L.bf_status_string(s).decode().startswith("BF_")
     assert bfmod.version().startswith("bf-b200")
 
@@ -122,11 +124,11 @@ def test_plan_edge_parameters(bfmod):
 
 
 def test_launch_count_query(bfmod):
-    """bf_apply_launches: one launch when the terms fit one pass, ceil(N / 16) at r = 192 (cfg4:
-    24 terms), argument validation; host-only (no device work)."""
+    """bf_apply_launches: one launch for every BASELINE config (cfg4's 24 terms at r = 192 split
+    over a 3-CTA cluster instead of two workspace passes), argument validation; host-only."""
     import ctypes as C
     L = bfmod.lib()
-    for cfg, want in (("cfg0", 1), ("cfg2", 1), ("cfg3", 1), ("cfg4", 2)):
+    for cfg, want in (("cfg0", 1), ("cfg2", 1), ("cfg3", 1), ("cfg4", 1)):
         p = config_params(CONFIGS[cfg])
         plan = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"],
                           sigma_r=p["sigma_r"], radius=p["radius"], n_terms=p["n_terms"],
@@ -137,44 +139,92 @@ def test_launch_count_query(bfmod):
     assert L.bf_apply_launches(plan.handle, 0, 4, C.byref(n)) == bfmod.BF_ERR_INVALID_ARG
 
 
-def test_launch_config_query(bfmod, monkeypatch):
-    """bf_apply_config describes the launches without device work: the fused warp-specialised
-    kernel (768 threads, at most 384 - halo output columns per strip, narrower strips where they
-    fill the SMs better) for the separable N_s = 9 plans, the
-    band kernel for cfg4's r = 192 halo (2 passes), the literal kernel for range_window='literal';
-    BF_KERNEL forces a kernel; the grid covers the image."""
+def test_launch_config_query(bfmod):
+    """bf_apply_config describes the launches without device work: kernel 2b (768 threads) for the
+    separable N_s = 9 plans, one column per vertical-pass thread and one CTA per strip while the
+    halo leaves a strip >= 256 wide (cfg0-cfg3); cfg4's r = 192 halo takes two columns per thread
+    (768 extended columns) and its 24 terms split over a cluster of 3 CTAs (8 terms each), one
+    launch and no workspace. The kernel argument forces kernels 1 / 2 (one pass per 8 or 16
+    terms, with a workspace); the literal kernel for range_window='literal'; the grid covers the
+    image."""
     import ctypes as C
-    for cfg, kern, launches in (("cfg2", "bf_ws2_kernel", 1), ("cfg1", "bf_ws2_kernel", 1),
-                                ("cfg4", "bf_band_kernel", 2)):
+    for cfg, cols, cluster in (("cfg2", 1, 1), ("cfg1", 1, 1), ("cfg0", 1, 1), ("cfg3", 1, 1), ("cfg4", 2, 3)):
         spec = CONFIGS[cfg]
         p = config_params(spec)
+        u8 = spec.gen == "ramp" and not spec.as_f32
         plan = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"],
                           sigma_r=p["sigma_r"], radius=p["radius"], n_terms=p["n_terms"],
-                          intensity_max=p["intensity_max"])
+                          intensity_max=p["intensity_max"], input_dtype="u8" if u8 else "f32")
         c = bfmod.config(plan, spec.H, spec.W)
-        assert c["kernel"] == kern and c["launches"] == launches == bfmod.launches(plan, spec.H, spec.W), cfg
+        assert c["kernel"] == "bf_ws2_kernel" and c["launches"] == 1 == bfmod.launches(plan, spec.H, spec.W), cfg
+        assert (c["cols_per_thread"], c["cluster"], c["workspace_bytes"]) == (cols, cluster, 0), (cfg, c)
         tw, th = c["tile"]
         gx, gy, gz = c["grid"]
-        assert gx * tw >= spec.W > (gx - 1) * tw and gy * th >= spec.H > (gy - 1) * th and gz == 1
-        assert c["smem_bytes"] <= 227 * 1024
-        if kern == "bf_ws2_kernel":
-            halo = 2 * p["radius"]
-            widest = min(320, 384 - halo)
-            assert c["threads_per_cta"] == 768 and (tw == widest or (tw % 32 == 0 and 128 <= tw < widest))
+        strips = gx // cluster
+        assert gx % cluster == 0 and strips * tw >= spec.W > (strips - 1) * tw and gy * th >= spec.H > (gy - 1) * th
+        assert gz == 1 and c["smem_bytes"] <= 227 * 1024 and c["threads_per_cta"] == 768
+        halo = 2 * p["radius"]
+        widest = min(320 if cols == 1 else 352, 384 * cols - halo)
+        assert tw == widest or (tw % 32 == 0 and 128 <= tw < widest), (cfg, tw)
+        if cluster > 1:
+            assert c["terms_per_cta"] * cluster >= len(plan.info()["k"]) > c["terms_per_cta"] * (cluster - 1)
     spec = CONFIGS["cfg2"]
     p = config_params(spec)
     plan = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"], sigma_r=p["sigma_r"],
                       radius=p["radius"], n_terms=p["n_terms"], intensity_max=p["intensity_max"])
     for k, name, threads in (("band", "bf_band_kernel", 256), ("ws", "bf_ws_kernel", 640)):
-        monkeypatch.setenv("BF_KERNEL", k)
-        c = bfmod.config(plan, 333, 361)
+        c = bfmod.config(plan, 333, 361, args=bfmod.make_args(kernel=k))
         assert (c["kernel"], c["threads_per_cta"], c["tile"][0]) == (name, threads, 256 - 2 * p["radius"])
-    monkeypatch.delenv("BF_KERNEL")
+    # cfg4 on kernel 1 (forced): two passes of 16 terms through a workspace of 16 B per pixel
+    p4 = config_params(CONFIGS["cfg4"])
+    plan4 = bfmod.Plan(spatial=p4["spatial"], range_kind=p4["range_kind"], sigma_s=p4["sigma_s"],
+                       sigma_r=p4["sigma_r"], radius=p4["radius"], n_terms=p4["n_terms"],
+                       intensity_max=p4["intensity_max"])
+    c = bfmod.config(plan4, 1000, 900, args=bfmod.make_args(kernel="band"))
+    assert c["kernel"] == "bf_band_kernel" and c["launches"] == 2 and c["workspace_bytes"] == 16 * 1000 * 900
+    assert bfmod.workspace_size(plan4, 1000, 900, args=bfmod.make_args(kernel="band")) == 16 * 1000 * 900
+    assert bfmod.workspace_size(plan4, 1000, 900) == 0
+    c = bfmod.config(plan, 100, 100, args=bfmod.make_args(band_rows=7))
+    assert c["tile"][1] == 7 and c["grid"][1] == 15
     lit = bfmod.Plan(range_window="literal", input_dtype="u8", radius=10, n_terms=4)
     assert bfmod.config(lit, 100, 100)["kernel"] == "bf_literal_kernel"
     c = bfmod.LaunchConfig()
-    assert bfmod.lib().bf_apply_config(None, 1, 4, 4, C.byref(c)) == bfmod.BF_ERR_INVALID_ARG
-    assert bfmod.lib().bf_apply_config(plan.handle, 0, 4, 4, C.byref(c)) == bfmod.BF_ERR_INVALID_ARG
+    assert bfmod.lib().bf_apply_config(None, 1, 4, 4, None, C.byref(c)) == bfmod.BF_ERR_INVALID_ARG
+    assert bfmod.lib().bf_apply_config(plan.handle, 0, 4, 4, None, C.byref(c)) == bfmod.BF_ERR_INVALID_ARG
+
+
+def test_multi_pass_plan_needs_workspace(bfmod):
+    """bf_apply never allocates: a plan that runs in several passes (here a forced kernel 1 on a
+    24-term plan, or a rank-2 N_s = 5 plan with 12 terms) returns BF_ERR_WORKSPACE without a
+    workspace, before any device work."""
+    import ctypes as C
+    L = bfmod.lib()
+    p = config_params(CONFIGS["cfg1"])
+    plan = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"], sigma_r=p["sigma_r"],
+                      radius=p["radius"], n_terms=p["n_terms"], n_spatial=5)
+    assert bfmod.config(plan, 64, 64)["launches"] == 2
+    assert L.bf_apply(plan.handle, C.c_void_p(16), C.c_void_p(4096), 64, 64, None) == bfmod.BF_ERR_WORKSPACE
+    a = bfmod.make_args(workspace=(8192, 100))
+    assert L.bf_apply_ex(plan.handle, C.c_void_p(16), C.c_void_p(4096), 1, 64, 64, None, C.byref(a)) == \
+        bfmod.BF_ERR_WORKSPACE
+
+
+def test_multi_plan_validation(bfmod):
+    """bf_apply_multi takes separable plans with at most two boxes per axis (N_s = 2 /
+    5 plans were silently wrong or failed late): others are BF_ERR_UNSUPPORTED before any device
+    work, and so is a union of more than 16 terms."""
+    import ctypes as C
+    L = bfmod.lib()
+    for ns in (5, 25):
+        a = bfmod.Plan(sigma_s=4.0, radius=12, n_terms=4, n_spatial=ns)
+        b = bfmod.Plan(sigma_s=4.0, radius=12, n_terms=4, n_spatial=ns, sigma_r=20.0)
+        arr = (C.c_void_p * 2)(a.handle.value, b.handle.value)
+        assert L.bf_apply_multi(arr, 2, C.c_void_p(16), C.c_void_p(4096), 32, 32, None) == bfmod.BF_ERR_UNSUPPORTED
+    a = bfmod.Plan(n_terms=12, sigma_r=10.0)
+    b = bfmod.Plan(n_terms=20, sigma_r=10.0)
+    assert len(set(a.info()["k"]) | set(b.info()["k"])) > 16
+    arr = (C.c_void_p * 2)(a.handle.value, b.handle.value)
+    assert L.bf_apply_multi(arr, 2, C.c_void_p(16), C.c_void_p(4096), 32, 32, None) == bfmod.BF_ERR_UNSUPPORTED
 
 
 def test_spatial_rank_of_the_gpu_form(bfmod):

@@ -36,9 +36,9 @@ def make_plans(pkg, params, dtype, **over):
     return gp, op
 
 
-def run_gpu(pkg, torch, plan, img):
+def run_gpu(pkg, torch, plan, img, **kw):
     t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
-    out = pkg.bilateral_filter(plan, t)
+    out = pkg.bilateral_filter(plan, t, **kw)
     torch.cuda.synchronize()
     return out.cpu().numpy().astype(np.float64)
 
@@ -191,7 +191,7 @@ def test_deterministic(gpu):
 
 
 @pytest.mark.parametrize("cfg,H,W", [("cfg0", 150, 230), ("cfg1", 170, 260), ("cfg2", 140, 250)])
-def test_rank2_three_box_plan(gpu, cfg, H, W, monkeypatch):
+def test_rank2_three_box_plan(gpu, cfg, H, W):
     """N_s = 5 (f1 + f2 + f3, the paper's three boxes): a rank-2 spatial kernel, run as two
     box-pair terms (NEXT f3). Both kernels, against the oracle's box evaluation of the same plan."""
     pkg, torch = gpu
@@ -207,8 +207,7 @@ def test_rank2_three_box_plan(gpu, cfg, H, W, monkeypatch):
     assert well.mean() > 0.99
     outs = []
     for k in ("band", "ws"):
-        monkeypatch.setenv("BF_KERNEL", k)
-        outs.append(run_gpu(pkg, torch, gp, img))
+        outs.append(run_gpu(pkg, torch, gp, img, kernel=k, repair_threshold=-1))
         assert np.all(np.isfinite(outs[-1]))
         assert_parity(outs[-1][well], ref[well], spec.intensity_max, f"{cfg} N_s=5 {k}")
     assert np.array_equal(outs[0], outs[1])
@@ -216,7 +215,7 @@ def test_rank2_three_box_plan(gpu, cfg, H, W, monkeypatch):
 
 @pytest.mark.parametrize("cfg,H,W", [("cfg0", 256, 256), ("cfg1", 150, 347), ("cfg2", 333, 361), ("cfg3", 211, 333),
                                      ("cfg1", 3, 500), ("cfg2", 97, 161)])
-def test_kernels_agree_bitwise(gpu, cfg, H, W, monkeypatch):
+def test_kernels_agree_bitwise(gpu, cfg, H, W):
     """The warp-specialised kernels (named-barrier pipelines, BF_KERNEL=ws / ws2) and the
     barrier-interval kernel (BF_KERNEL=band) perform the same exact integer arithmetic with different schedules and
     walker segmentations: their outputs must be bitwise equal (a synchronisation race would show)."""
@@ -226,8 +225,7 @@ def test_kernels_agree_bitwise(gpu, cfg, H, W, monkeypatch):
     gp, op = make_plans(pkg, config_params(spec), img.dtype)
     outs = {}
     for k in ("band", "ws", "ws2"):
-        monkeypatch.setenv("BF_KERNEL", k)
-        outs[k] = run_gpu(pkg, torch, gp, img)
+        outs[k] = run_gpu(pkg, torch, gp, img, kernel=k)
     assert np.array_equal(outs["band"], outs["ws"])
     assert np.array_equal(outs["band"], outs["ws2"])
     assert_parity(outs["ws2"], bf.bf_box(img, op), spec.intensity_max, cfg)
@@ -236,7 +234,7 @@ def test_kernels_agree_bitwise(gpu, cfg, H, W, monkeypatch):
 @pytest.mark.parametrize("cfg,H,W,over", [("cfg1", 140, 300, {"range_kind": "tukey", "sigma_r": 40.0, "n_terms": 12}),
                                           ("cfg0", 120, 250, {"range_kind": "tukey", "sigma_r": 40.0, "n_terms": 13}),
                                           ("cfg2", 150, 330, {"n_terms": 5})])
-def test_kernels_agree_nonconsecutive_and_partial(gpu, cfg, H, W, over, monkeypatch):
+def test_kernels_agree_nonconsecutive_and_partial(gpu, cfg, H, W, over):
     """Tukey plans select non-consecutive k (the CONSEC = false instantiations, a runtime
     recurrence step count per term) and N_eff < MAXK leaves a partial channel group (FULL =
     false): the three kernels agree bitwise there too, and match the oracle."""
@@ -249,8 +247,7 @@ def test_kernels_agree_nonconsecutive_and_partial(gpu, cfg, H, W, over, monkeypa
         assert any(b - a > 1 for a, b in zip(ks, ks[1:])), ks
     outs = {}
     for k in ("band", "ws", "ws2"):
-        monkeypatch.setenv("BF_KERNEL", k)
-        outs[k] = run_gpu(pkg, torch, gp, img)
+        outs[k] = run_gpu(pkg, torch, gp, img, kernel=k)
     assert np.array_equal(outs["band"], outs["ws"]) and np.array_equal(outs["band"], outs["ws2"])
     assert_parity(outs["ws2"], bf.bf_box(img, op), spec.intensity_max, cfg)
 
@@ -283,7 +280,7 @@ def test_multi_plan_case1_shared_channels(gpu):
 @pytest.mark.parametrize("cfg,H,W", [("cfg0", 300, 256), ("cfg2", 260, 300), ("cfg3", 200, 240),
                                      ("cfg4", 420, 300)])
 @pytest.mark.parametrize("kernel", ["band", "ws", "ws2"])
-def test_sliding_sums_are_exact(gpu, cfg, H, W, kernel, monkeypatch):
+def test_sliding_sums_are_exact(gpu, cfg, H, W, kernel):
     """The vertical state slides by adding the quantised enter taps and subtracting the leave
     taps, which must cancel EXACTLY (the leave tap regenerates bit for bit what the enter tap, or
     the band's initial sum, added). Every band restarts from a fresh initial sum, so the output
@@ -293,18 +290,16 @@ def test_sliding_sums_are_exact(gpu, cfg, H, W, kernel, monkeypatch):
     spec = CONFIGS[cfg]
     img = config_input(spec, H=H, W=W)
     gp, _ = make_plans(pkg, config_params(spec), img.dtype)
-    monkeypatch.setenv("BF_KERNEL", kernel)
     outs = []
-    for th in ("16", str(H)):
-        monkeypatch.setenv("BF_TH", th)
-        outs.append(run_gpu(pkg, torch, gp, img))
+    for th in (16, H):
+        outs.append(run_gpu(pkg, torch, gp, img, kernel=kernel, band_rows=th))
     assert np.array_equal(outs[0], outs[1])
 
 
 @pytest.mark.parametrize("cfg,H,W,over", [("cfg0", 160, 230, {}), ("cfg3", 120, 260, {}),
                                           ("cfg0", 100, 140, {"range_kind": "tukey", "sigma_r": 40.0}),
                                           ("cfg0", 70, 90, {"n_terms": 3})])
-def test_literal_window_parity(gpu, cfg, H, W, over, monkeypatch):
+def test_literal_window_parity(gpu, cfg, H, W, over):
     """NEXT f1, the paper's literal 3-D box filter (window [I(x) - T_r, I(x) + T_r]) on u8 images:
     the level-count kernel against the oracle's dimension-promoted evaluation of the same plan;
     integer counts make the result independent of the band height (bitwise)."""
@@ -320,8 +315,7 @@ def test_literal_window_parity(gpu, cfg, H, W, over, monkeypatch):
     ref = bf.bf_promoted(img.astype(np.float64), op, Tr)[0]
     got = run_gpu(pkg, torch, gp, img)
     assert_parity(got, ref, 255.0, f"{cfg} literal {over}")
-    monkeypatch.setenv("BF_TH", "16")
-    assert np.array_equal(run_gpu(pkg, torch, gp, img), got)
+    assert np.array_equal(run_gpu(pkg, torch, gp, img, band_rows=16), got)
 
 
 @pytest.mark.parametrize("cfg,over", [("cfg1", {"sigma_r": 10.0}), ("cfg0", {"sigma_r": 10.0, "n_terms": 12}),
