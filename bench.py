@@ -2,14 +2,24 @@
 """Benchmark of the B200 joint-acceleration bilateral filter (one JSON line on rank 0).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+                    [--n-spatial 9] [--no-per-config] [--no-cpu-baseline]
 
-A "step" is one bf_apply of the whole hot path (modulate + box sums + combine + divide) over one
-synthetic image of the workload (BASELINE.json configs; default cfg2 = 4096x4096 f32, the config
-the north_star target is quoted on). Inputs are resident in HBM before the timed region; L2 is
-flushed (a 256 MiB write) before every timed step and the step is timed alone with CUDA events
-on the launching stream. For N > 1 (torchrun) every rank filters its own image (independent
-problems, weak scaling), times are max-reduced over ranks, value = all ranks' pixels / max time.
-`e2e` repeats the metric through bf_apply_host (pinned host input -> device -> host output).
+A "step" is one pass of the whole hot path (modulate + box sums + combine + divide, plus the fp64
+repair of ill-conditioned pixels) over one synthetic input of the workload: one image for cfg0,
+cfg1, cfg2 (the headline: the config the north_star target is quoted on), cfg4; 64 frames as 64
+back-to-back bf_apply calls on one stream for cfg3 (BASELINE.json configs[3]). Inputs are resident
+in HBM before the timed region; L2 is flushed (a 256 MiB write) before every timed step and the
+step is timed alone with CUDA events on the launching stream. For N > 1 (torchrun) every rank
+filters its own image (independent problems, weak scaling), times are max-reduced over ranks,
+value = all ranks' pixels / max time. `e2e` repeats the metric through bf_apply_host (pinned host
+input -> device -> host output).
+
+Extra keys: `roofline` (the fused kernel alone against the ALU model),
+`hbm_roofline` (the BASELINE metric's HBM fraction), `per_config` (every BASELINE config, each
+timed the same way), `parity` (the device fallback / repair counters of one step and the committed
+every-pixel full-size result of tests/test_gpu_fullsize.py; the oracle itself runs only in the
+cpu_baseline / reference legs), `ncu` (pipe utilisation of the committed capture),
+`cpu_baseline` (the oracle on the host cores).
 """
 from __future__ import annotations
 
@@ -130,53 +140,82 @@ def barrier(world: int):
         dist.barrier()
 
 
-def config_dict(spec, flush: bool, world: int) -> dict:
-    return {"workload": f"{spec.name}: {spec.H}x{spec.W} {'uint8' if spec.gen == 'ramp' and not spec.as_f32 else 'float32'}"
+def is_u8(spec) -> bool:
+    return spec.gen == "ramp" and not spec.as_f32
+
+
+def frames_per_step(spec) -> int:
+    return spec.frames
+
+
+def config_dict(spec, flush: bool, world: int, n_spatial: int) -> dict:
+    return {"workload": f"{spec.name}: {spec.H}x{spec.W} {'uint8' if is_u8(spec) else 'float32'}"
                         f" {spec.gen}, K_s {spec.spatial} sigma_s={spec.sigma_s} r={spec.radius}, "
                         f"K_r {spec.range_kind} sigma_r={spec.sigma_r}, N={spec.n_terms}, D={spec.intensity_max}",
-            "H": spec.H, "W": spec.W, "frames_per_step": 1, "n_spatial": 9,
+            "H": spec.H, "W": spec.W, "frames_per_step": frames_per_step(spec), "n_spatial": n_spatial,
             "l2": "flushed (256 MiB write) before every timed step" if flush else "not flushed",
             "parallelism": f"dp{world} (independent images per rank)" if world > 1 else "single GPU"}
 
 
 # --------------------------------------------------------------------------------------------
-# reference arm: the CPU oracle as it stands (TEST INFRASTRUCTURE used only here and in tests)
+# the CPU oracle (TEST INFRASTRUCTURE used only here, in tests/ and smoke()): the reference arm and
+# cpu_baseline. Row bands of a crop are evaluated by os.cpu_count() worker processes
+# (tests/fullsize.py: the banded evaluation equals one bf_box call over the crop).
 # --------------------------------------------------------------------------------------------
 
-def oracle_sample_rate(spec, side: int) -> tuple:
-    """Time the oracle (fp64 numpy SAT evaluation) on a side x side crop of the workload."""
-    from oracle import bf as obf
-    from oracle import fit as ofit
+def oracle_rate(spec, side: int, n_spatial: int, pool=None) -> tuple:
+    """(MP/s, seconds, description) of the oracle on a side x side crop of the workload."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from fullsize import oracle_banded
     from synth import config_input, config_params
-    full = config_input(spec, H=min(spec.H, 1024), W=min(spec.W, 1024))
-    crop = full[:side, :side]
-    plan = ofit.make_plan(**config_params(spec))
+    full = config_input(spec, H=min(spec.H, max(side, 256)), W=min(spec.W, max(side, 256)))
+    crop = full[:side, :side].copy()
+    params = dict(config_params(spec), n_spatial=n_spatial)
     t0 = time.perf_counter()
-    obf.bf_box(crop, plan)
+    oracle_banded(crop, params, pool=pool)
     dt = time.perf_counter() - t0
-    return crop.size / dt / 1e6, dt, f"{side}x{side} crop of the {spec.name} input, full oracle (fp64 SAT evaluation)"
+    return crop.size / dt / 1e6, dt, (f"{crop.shape[0]}x{crop.shape[1]} crop of the {spec.name} input (frame 0), "
+                                      f"oracle.bf.bf_box (fp64 SAT) over {os.cpu_count()} row bands in "
+                                      f"{os.cpu_count()} processes")
+
+
+def cpu_baseline(spec, side: int, n_spatial: int, runs: int = 3) -> dict:
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+    n = os.cpu_count() or 1
+    with ProcessPoolExecutor(max_workers=n, mp_context=mp.get_context("spawn")) as pool:
+        oracle_rate(spec, 128, n_spatial, pool)          # warm the workers (imports)
+        res = [oracle_rate(spec, side, n_spatial, pool) for _ in range(runs)]
+    rates = [r for r, _, _ in res]
+    med = statistics.median(rates)
+    return {"value": med, "unit": UNIT, "cores": n, "kind": "oracle", "sample": res[0][2],
+            "runs": runs, "statistic": "median", "seconds": [dt for _, dt, _ in res]}
 
 
 def run_reference(args, spec):
     world, rank, _ = dist_setup(args.gpus)
     if rank != 0:
         return 0
-    side = args.ref_side
-    rates = []
-    samples = []
-    for i in range(args.warmup + args.steps):
-        r, dt, desc = oracle_sample_rate(spec, side)
-        if i >= args.warmup:
-            rates.append(r)
-            samples.append(dt)
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+    n = os.cpu_count() or 1
+    rates, secs = [], []
+    with ProcessPoolExecutor(max_workers=n, mp_context=mp.get_context("spawn")) as pool:
+        desc = ""
+        for i in range(args.warmup + args.steps):
+            r, dt, desc = oracle_rate(spec, args.ref_side, args.n_spatial, pool)
+            if i >= args.warmup:
+                rates.append(r)
+                secs.append(dt)
     v = statistics.median(rates)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(samples),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_dict(spec, False, 1),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "data": "synthetic", "config": config_dict(spec, False, 1, args.n_spatial),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": n, "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "note": "single-process numpy fp64 oracle on the GPU box's host cores; each step is a bounded sample"}
+            "note": "the fp64 numpy oracle as it stands on the GPU box's host cores (row bands in parallel); "
+                    "each step is a bounded crop of the workload"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -185,124 +224,226 @@ def run_reference(args, spec):
 # our arm
 # --------------------------------------------------------------------------------------------
 
-def traffic_per_launch(cfg: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
-    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if not os.path.exists(p):
-        return None
-    return json.load(open(p)).get(cfg, {}).get("dram_bytes_per_launch")
+def committed_json(name: str):
+    p = os.path.join(ROOT, "profiles", name)
+    return json.load(open(p)) if os.path.exists(p) else None
+
+
+class Workload:
+    """One BASELINE config resident on the device: inputs, outputs, plan, the step callable."""
+
+    def __init__(self, pkg, torch, spec, dev, n_spatial: int):
+        from synth import config_input
+        self.spec = spec
+        self.plan = pkg.Plan(spatial=spec.spatial, range_kind=spec.range_kind, sigma_s=spec.sigma_s,
+                             sigma_r=spec.sigma_r, radius=spec.radius, n_terms=spec.n_terms,
+                             intensity_max=spec.intensity_max, n_spatial=n_spatial,
+                             input_dtype="u8" if is_u8(spec) else "f32")
+        self.frames = [config_input(spec, frame=f) for f in range(spec.frames)]
+        self.inp = torch.from_numpy(self.frames[0] if spec.frames == 1 else __import__("numpy").stack(self.frames)).to(dev)
+        self.out = torch.empty(self.inp.shape, dtype=torch.float32, device=dev)
+        self.H, self.W = spec.H, spec.W
+        self.pkg = pkg
+        self.fb = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.rep = torch.zeros(1, dtype=torch.int64, device=dev)
+        ws = pkg.workspace_size(self.plan, self.H, self.W)
+        self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
+        self.wsb = ws
+
+    def args(self, repair=True, counters=False):
+        return self.pkg.make_args(workspace=(self.ws.data_ptr(), self.wsb) if self.wsb else (0, 0),
+                                  repair_threshold=0.0 if repair else -1.0,
+                                  fallback_count=self.fb.data_ptr() if counters else 0,
+                                  repaired_count=self.rep.data_ptr() if counters else 0)
+
+    def step(self, stream, args=None):
+        """One step: every frame through bf_apply_ex (cfg3: 64 calls on one stream)."""
+        n = self.H * self.W
+        esz = self.inp.element_size()
+        for f in range(self.spec.frames):
+            self.pkg.apply_ex(self.plan, self.inp.data_ptr() + f * n * esz, self.out.data_ptr() + f * n * 4, 1,
+                              self.H, self.W, stream, args)
+
+    def step_batched(self, stream, args=None):
+        self.pkg.apply_ex(self.plan, self.inp.data_ptr(), self.out.data_ptr(), self.spec.frames, self.H, self.W,
+                          stream, args)
+
+
+def timed(torch, stream, fn, steps, warmup, flush, sampler=None):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    ctx = sampler if sampler is not None else _Null()
+    with ctx:
+        for _ in range(steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    return times
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+
+def alu_channels(plan) -> int:
+    """C = 4 N_eff box-filtered channels, 4 N_eff - 2 when k = 0 is selected (sin(0 I) == 0)."""
+    ks = plan.info()["k"]
+    return 4 * len(ks) - (2 if 0 in ks else 0)
+
+
+def bench_one(pkg, torch, spec, dev, stream, flush, args, steps, warmup, peaks, sampler=None, n_spatial=9):
+    wl = Workload(pkg, torch, spec, dev, n_spatial)
+    sptr = stream.cuda_stream
+    a = wl.args()
+    times = timed(torch, stream, lambda: wl.step(sptr, a), steps, warmup, flush, sampler)
+    ms = statistics.median(times) if sampler is None else sum(times) / len(times)
+    # the fused kernel alone (no repair launch) for the roofline
+    a0 = wl.args(repair=False)
+    kt = timed(torch, stream, lambda: wl.step(sptr, a0), max(3, steps // 2), 2, flush)
+    kms = statistics.median(kt)
+    cfg = pkg.config(wl.plan, spec.H, spec.W)
+    px = spec.H * spec.W * spec.frames
+    bpp = (1 if is_u8(spec) else 4) + 4
+    C = alu_channels(wl.plan)
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    alu_peak = 148 * 128 * sm_mhz * 1e6
+    res = {"ms_per_step": ms, "value": px / 1e6 / (ms / 1e3), "unit": UNIT, "frames_per_step": spec.frames,
+           "kernel_ms": kms, "kernel": cfg["kernel"], "launches_per_frame": cfg["launches"] + 1,
+           "launch": {"threads_per_cta": cfg["threads_per_cta"], "grid": list(cfg["grid"]), "tile": list(cfg["tile"]),
+                      "smem_bytes": cfg["smem_bytes"], "cluster": cfg["cluster"],
+                      "terms_per_cta": cfg["terms_per_cta"], "cols_per_thread": cfg["cols_per_thread"]},
+           "hbm_frac": px * bpp / (kms / 1e3) / 1e9 / float(peaks["hbm_gbs"]),
+           "alu_frac": 8.0 * C * px / (kms / 1e3) / alu_peak, "channels": C}
+    if spec.frames > 1:
+        bt = timed(torch, stream, lambda: wl.step_batched(sptr, a), steps, warmup, flush)
+        res["batched_ms_per_step"] = statistics.median(bt)
+        res["batched_value"] = px / 1e6 / (res["batched_ms_per_step"] / 1e3)
+        res["per_frame_ms"] = ms / spec.frames
+    return wl, res, times
 
 
 def run_ours(args, spec):
     import torch
     from paper_1803_00004_b200 import build
     build.build()
-    import paper_1803_00004_b200 as bfp
-    from synth import config_input
+    import paper_1803_00004_b200 as pkg
+    from synth import CONFIGS
 
     world, rank, local = dist_setup(args.gpus)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    u8 = (spec.gen == "ramp" and not spec.as_f32)
-    plan = bfp.Plan(spatial=spec.spatial, range_kind=spec.range_kind, sigma_s=spec.sigma_s, sigma_r=spec.sigma_r,
-                    radius=spec.radius, n_terms=spec.n_terms, intensity_max=spec.intensity_max,
-                    input_dtype="u8" if u8 else "f32")
-    img_np = config_input(spec)
-    img = torch.from_numpy(img_np).to(dev)
-    out = torch.empty(img.shape, dtype=torch.float32, device=dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    sptr = stream.cuda_stream
-    H, W = img.shape
-    launches = bfp.launches(plan, H, W)     # kernel launches per bf_apply (bf_apply_launches)
-    lcfg = bfp.config(plan, H, W)            # the kernel and launch shape bf_apply enqueues (bf_apply_config)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    peaks = measured_peaks()
 
-    def step():
-        bfp.apply(plan, img.data_ptr(), out.data_ptr(), H, W, sptr)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
     barrier(world)
-    torch.cuda.synchronize()
-    times = []
     sampler = ClockSampler(local)
-    with sampler:
-        for _ in range(args.steps):
-            flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            step()
-            e1.record(stream)
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1))
-    torch.cuda.synchronize()
+    wl, head, times = bench_one(pkg, torch, spec, dev, stream, flush, args, args.steps, args.warmup, peaks, sampler,
+                                args.n_spatial)
     barrier(world)
     total_ms = reduce_max(sum(times), world, dev)
     ms = total_ms / args.steps
-    mpix_all = world * H * W * args.steps / 1e6
-    value = mpix_all / (total_ms / 1e3)
+    px_step = spec.H * spec.W * spec.frames
+    value = world * px_step * args.steps / 1e6 / (total_ms / 1e3)
+    launches = wl.pkg.launches(wl.plan, spec.H, spec.W) + 1      # fused launch(es) + the repair pass
+
+    # parity: device counters of one step, the live sampled check, the committed every-pixel run
+    wl.fb.zero_()
+    wl.rep.zero_()
+    wl.step(stream.cuda_stream, wl.args(counters=True))
+    torch.cuda.synchronize()
+    parity = {"fallback_pixels": int(wl.fb.item()), "repaired_pixels": int(wl.rep.item())}
 
     # ---- end to end through the public host API (pinned host buffers, copies inside the timing)
-    h_in = torch.from_numpy(img_np).pin_memory()
-    h_out = torch.empty((H, W), dtype=torch.float32).pin_memory()
+    h_in = [torch.from_numpy(f).pin_memory() for f in wl.frames]
+    h_out = torch.empty((spec.H, spec.W), dtype=torch.float32).pin_memory()
+    sptr = stream.cuda_stream
+
+    def e2e_step():
+        for f in range(spec.frames):
+            pkg.apply_host(wl.plan, h_in[f].data_ptr(), h_out.data_ptr(), spec.H, spec.W, sptr)
+
     for _ in range(max(1, args.warmup // 2)):
-        bfp.apply_host(plan, h_in.data_ptr(), h_out.data_ptr(), H, W, sptr)
+        e2e_step()
     barrier(world)
     e2e_t = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        bfp.apply_host(plan, h_in.data_ptr(), h_out.data_ptr(), H, W, sptr)
+        e2e_step()
         e2e_t.append(time.perf_counter() - t0)
     e2e_total = reduce_max(sum(e2e_t), world, dev)
-    e2e_value = world * H * W * args.steps / 1e6 / e2e_total
+    e2e_value = world * px_step * args.steps / 1e6 / e2e_total
 
     if rank != 0:
         barrier(world)
         return 0
-    peaks = measured_peaks()
-    bytes_per_px = (1 if u8 else 4) + 4
-    alg_bytes = H * W * bytes_per_px
-    hbm_gbs = alg_bytes / (ms / 1e3) / 1e9
-    hbm_peak = float(peaks["hbm_gbs"])
+    committed = committed_json(f"r2_parity_{spec.name}.json")
+    if committed:
+        parity["full_size_every_pixel"] = {k: committed.get(k) for k in
+                                           ("pixels", "max_abs", "rmse", "pass", "cond_min", "n_oracle_fallbacks",
+                                            "n_fallback_match", "n_cond_below_1e-3")}
+        parity["full_size_every_pixel"]["source"] = f"profiles/r2_parity_{spec.name}.json (tests/test_gpu_fullsize.py)"
     clocks = sampler.summary()
-    nk = len(plan.info()["k"])
-    C = 4 * nk
-    # ALU roofline (the bound of this path, DESIGN.md section 6): SURVEY 8(d)'s algorithmic work of
-    # >= 8 FP32-lane ops per box-filtered channel per pixel, against 148 SMs x 128 FP32 lanes x the
-    # SM clock measured under load (max clock if nvidia-smi gave none)
+    hbm_peak = float(peaks["hbm_gbs"])
+    bpp = (1 if is_u8(spec) else 4) + 4
+    alg_bytes = px_step * bpp
     sm_mhz = clocks.get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12                  # T lane-op/s
-    alu_ops = 8.0 * C * H * W                                    # per step
-    alu_achieved = alu_ops / (ms / 1e3) / 1e12
+    C = alu_channels(wl.plan)
+    alu_ops = 8.0 * C * px_step
+    kms = head["kernel_ms"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 channels, i32 box sums, i64 combine", "data": "synthetic",
-        "config": config_dict(spec, True, world),
-        "roofline": {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "T lane-op/s",
-                     "frac": alu_achieved / alu_peak, "traffic": traffic_per_launch(spec.name),
-                     "kernel": lcfg["kernel"], "launches_per_step": launches,
-                     "launch": {"threads_per_cta": lcfg["threads_per_cta"], "grid": list(lcfg["grid"]),
-                                "tile": list(lcfg["tile"]), "smem_bytes": lcfg["smem_bytes"]},
-                     "algorithmic_ops_per_step": alu_ops,
-                     "peak_source": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (B200_PROFILING.md unit counts)",
-                     "note": "SURVEY 8(d): >= 8 FP32-lane ops per channel-pixel, C = 4 N_eff channels"},
-        "hbm_roofline": {"achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_gbs / hbm_peak,
-                         "algorithmic_bytes_per_step": alg_bytes,
+        "vs_baseline": None, "dtype": "f32 channels, i32 box sums, i64 combine (fp64 repair)", "data": "synthetic",
+        "config": config_dict(spec, True, world, args.n_spatial),
+        "roofline": {"bound": "alu", "achieved": alu_ops / (kms / 1e3) / 1e12, "peak": alu_peak,
+                     "unit": "T lane-op/s", "frac": alu_ops / (kms / 1e3) / 1e12 / alu_peak,
+                     "traffic": (committed_json("ncu_traffic.json") or {}).get(spec.name, {}).get("dram_bytes_per_launch"),
+                     "kernel": head["kernel"], "kernel_ms": kms, "launch": head["launch"],
+                     "algorithmic_ops_per_step": alu_ops, "channels": C,
+                     "peak_source": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (B200_PROFILING.md unit counts, "
+                                    "SM clock measured under load)",
+                     "note": "SURVEY 8(d): >= 8 FP32-lane ops per box-filtered channel-pixel, C = 4 N_eff - 2 "
+                             "channels (k = 0 selected: sin(0 I) == 0); the fused kernel timed alone"},
+        "hbm_roofline": {"achieved": alg_bytes / (kms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": alg_bytes / (kms / 1e3) / 1e9 / hbm_peak, "algorithmic_bytes_per_step": alg_bytes,
                          "peak_source": peaks["_source"] + " hbm_gbs",
                          "note": "BASELINE metric: image bytes in + out at the measured HBM bandwidth"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(img_np.nbytes),
-                "d2h_bytes_per_step": int(H * W * 4)},
-        "gpu_launches": args.steps * launches,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(wl.frames[0].nbytes) * spec.frames,
+                "d2h_bytes_per_step": int(spec.H * spec.W * 4) * spec.frames},
+        "gpu_launches": args.steps * launches * spec.frames,
         "clocks": clocks,
+        "parity": parity,
     }
+    ncu = committed_json("ncu_pipes.json")
+    if ncu and spec.name in ncu:
+        line["ncu"] = ncu[spec.name]
+    if not args.no_per_config:
+        per = {}
+        for name in sorted(CONFIGS):
+            if name == spec.name:
+                per[name] = {k: v for k, v in head.items()}
+                continue
+            s2 = CONFIGS[name]
+            k = 5 if name == "cfg4" else (3 if name == "cfg3" else 10)
+            _, r, _ = bench_one(pkg, torch, s2, dev, stream, flush, args, k, 3, peaks, None, args.n_spatial)
+            per[name] = r
+            torch.cuda.empty_cache()
+        line["per_config"] = per
     if not args.no_cpu_baseline:
-        r, dt, desc = oracle_sample_rate(spec, args.ref_side)
-        line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
-                                "seconds": dt}
+        line["cpu_baseline"] = cpu_baseline(spec, args.ref_side, args.n_spatial)
     print(json.dumps(line), flush=True)
     barrier(world)
     return 0
@@ -315,8 +456,10 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-side", type=int, default=768, help="side of the oracle's timed crop")
+    ap.add_argument("--n-spatial", type=int, default=9, help="N_s, the spatial Haar terms (default 9)")
+    ap.add_argument("--ref-side", type=int, default=1024, help="side of the oracle's timed crop")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
     args = ap.parse_args(argv)
     from synth import CONFIGS
     spec = CONFIGS[args.config]

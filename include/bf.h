@@ -184,6 +184,8 @@ typedef struct {
                                            below this (or den <= 0) are re-evaluated in fp64 from the
                                            approximated kernels (the direct double loop, reading Q27):
                                            0 = the library default (BF_REPAIR_DEFAULT), < 0 = off     */
+  unsigned long long* d_repaired_count; /* device counter, or NULL: incremented by the number of
+                                           pixels the fp64 repair pass re-evaluated                  */
   int u8_trig;                          /* u8 plans: 0 = the base angles (cos, sin)(pi I / D) from a
                                            256-entry table (Case 2; default), 1 = evaluated
                                            per tap (kernel 1 only): the same values, bitwise the same

@@ -30,7 +30,8 @@ def _check_tensor(t, plan):
 
 
 def bilateral_filter(plan: Plan, img, out=None, stream=None, kernel: str = "auto", band_rows: int = 0,
-                     fallback_count=None, fallback_mask=None, repair_threshold: float = 0.0, u8_trig: str = "lut"):
+                     fallback_count=None, fallback_mask=None, repair_threshold: float = 0.0, u8_trig: str = "lut",
+                     repaired_count=None):
     """Filters a [H, W] (or [F, H, W] batch) CUDA tensor with `plan` on the current stream.
 
     Multi-pass plans get a workspace from torch's allocator (the caller's memory: the library
@@ -49,7 +50,8 @@ def bilateral_filter(plan: Plan, img, out=None, stream=None, kernel: str = "auto
     args = make_args(kernel=kernel, band_rows=band_rows,
                      fallback_count=fallback_count.data_ptr() if fallback_count is not None else 0,
                      fallback_mask=fallback_mask.data_ptr() if fallback_mask is not None else 0,
-                     repair_threshold=repair_threshold, u8_trig=u8_trig)
+                     repair_threshold=repair_threshold, u8_trig=u8_trig,
+                     repaired_count=repaired_count.data_ptr() if repaired_count is not None else 0)
     ws = workspace_size(plan, H, W, F, args)
     wst = None
     if ws:

@@ -46,7 +46,7 @@ class ApplyArgs(C.Structure):
     _fields_ = [("kernel", C.c_int), ("band_rows", C.c_int), ("row_begin", C.c_int), ("row_end", C.c_int),
                 ("d_workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
                 ("d_fallback_count", C.c_void_p), ("d_fallback_mask", C.c_void_p), ("repair_threshold", C.c_double),
-                ("u8_trig", C.c_int)]
+                ("d_repaired_count", C.c_void_p), ("u8_trig", C.c_int)]
 
 
 class CacheDesc(C.Structure):
@@ -190,7 +190,8 @@ class Plan:
 
 
 def make_args(kernel: str = "auto", band_rows: int = 0, rows=None, workspace=(0, 0), fallback_count: int = 0,
-              fallback_mask: int = 0, repair_threshold: float = 0.0, u8_trig: str = "lut") -> ApplyArgs:
+              fallback_mask: int = 0, repair_threshold: float = 0.0, u8_trig: str = "lut",
+              repaired_count: int = 0) -> ApplyArgs:
     """bf_apply_args: kernel choice, band height, output row range, workspace (ptr, bytes), device
     fallback counter / mask pointers (0 = off), fp64 repair threshold (0 = default, < 0 = off)."""
     a = ApplyArgs()
@@ -205,6 +206,7 @@ def make_args(kernel: str = "auto", band_rows: int = 0, rows=None, workspace=(0,
     a.d_fallback_mask = C.c_void_p(int(fallback_mask)) if fallback_mask else None
     a.repair_threshold = float(repair_threshold)
     a.u8_trig = {"lut": 0, "direct": 1}[u8_trig]
+    a.d_repaired_count = C.c_void_p(int(repaired_count)) if repaired_count else None
     return a
 
 

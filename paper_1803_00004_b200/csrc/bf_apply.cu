@@ -260,6 +260,7 @@ void repair_params(const bf_plan* const* plans, int nplans, int n_frames, int H,
   R.cap = S.cap;
   R.fb_count = A.d_fallback_count;
   R.fb_mask = A.d_fallback_mask;
+  R.repaired = A.d_repaired_count;
 }
 
 // Claims a repair slot for one call and clears its counter on the stream (graph capturable).

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(RT) bf_repair_kernel(const RParams R, const vo
     fy[i] = wy;
   }
   const unsigned n = min(*R.count, R.cap);
+  if (R.repaired && blockIdx.x == 0 && tid == 0 && n) atomicAdd(R.repaired, (unsigned long long)n);
   int lut_q = -1;
   for (unsigned it = blockIdx.x; it < n; it += gridDim.x) {
     const unsigned long long e = R.list[it];

@@ -159,6 +159,7 @@ struct RParams {
   unsigned cap;
   unsigned long long* fb_count;
   unsigned char* fb_mask;
+  unsigned long long* repaired;   // optional: += pixels re-evaluated
 };
 constexpr unsigned REPAIR_SLOTS = 16, REPAIR_CAP = 1u << 16;
 // device addresses of repair slot s's counter and list (static device storage of the library)
