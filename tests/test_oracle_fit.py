@@ -226,3 +226,29 @@ def test_spatial_selection_never_splits_tie_group():
     keys = [fit.canonical_key(a, b) for a, b, _ in sp.terms]
     assert keys == sorted(keys) and len(keys) == 3
     assert sp.terms[0][0] == fit.PHI and sp.terms[0][1] == fit.PHI
+
+
+@pytest.mark.parametrize("kind,sigma", [("gaussian", 20.0), ("gaussian", 0.1), ("tukey", 40.0), ("tukey", 7.5)])
+def test_truncation_radius_is_the_eps_level_of_the_kernel(kind, sigma):
+    """T_r = K_r^{-1}(eps) (eps = 0.01): evaluated through the kernel itself, not through a
+    second copy of the inverse formula: K_r(T_r) = eps and K_r decreasing through it."""
+    T = fit.truncation_radius(kind, sigma)
+    K = fit.range_kernel(kind, sigma)
+    assert abs(float(K(T)) - 0.01) <= 1e-12
+    assert float(K(0.999 * T)) > 0.01 > float(K(1.001 * T))
+
+
+def test_canonical_key_orders_a_hand_written_list():
+    """Canonical order: family first (phi.phi, phi(x)psi(y), psi(x)phi(y),
+    psi.psi, eq:Haar_expansion P:304-307), then (j1, k1) of the x factor, then (j2, k2); phi sorts
+    before every psi. The expected order is written out by hand."""
+    P, s = fit.PHI, lambda j, k: ("psi", j, k)
+    expected = [
+        (P, P),
+        (P, s(0, 0)), (P, s(1, -1)), (P, s(1, 1)), (P, s(2, -2)),
+        (s(0, 0), P), (s(1, -1), P), (s(2, 1), P),
+        (s(0, 0), s(0, 0)), (s(0, 0), s(1, 1)), (s(1, -1), s(0, 0)), (s(1, -1), s(2, -2)),
+        (s(1, 1), s(0, 0)), (s(2, -2), s(1, -1)),
+    ]
+    shuffled = [expected[i] for i in (13, 2, 7, 0, 10, 5, 12, 1, 9, 3, 11, 6, 4, 8)]
+    assert sorted(shuffled, key=lambda t: fit.canonical_key(*t)) == expected
