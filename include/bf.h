@@ -135,8 +135,14 @@ typedef struct {
   double intensity_max;                      /* D                                              */
   int input_dtype;                           /* bf_input_dtype                                 */
   int spatial_rank;                          /* terms fx_s(u) fy_s(v) of the GPU box-pair form:
-                                                1 separable, 2 rank-2 (e.g. N_s = 5), 0 none     */
+                                                1 separable, 2 rank-2 (e.g. N_s = 5), R for the
+                                                general plans below, 0 none                       */
   int range_window;                          /* bf_plan_options.range_window of the plan        */
+  int spatial_passes;                        /* separable passes bf_apply runs: 1, or for general
+                                                plans (no separable / rank-2 form, e.g. N_s = 13
+                                                or 25 at haar_levels 4) one per product of box
+                                                groups of an exact rank-R factorisation (<= 16);
+                                                0 = no GPU form (BF_ERR_UNSUPPORTED)              */
 } bf_plan_info;
 
 /* Copies the plan contents into *info. */
@@ -192,11 +198,13 @@ typedef struct {
                                            output                                            */
 } bf_apply_args;
 
-/* Default bf_apply_args.repair_threshold: out = num / den magnifies the integer format's rounding
- * (relative ~1e-8 of the full-window denominator) by 1 / cond; below cond = 0.015 that can reach
- * the 1e-3 parity tolerance on the [0, 255] scale (measured on BASELINE cfg4 at 8192^2). At most
- * 65536 flagged pixels per call are repaired; up to 16 calls may be in flight per device. */
-#define BF_REPAIR_DEFAULT 0.015
+/* Default bf_apply_args.repair_threshold: out = num / den magnifies the fused kernels' rounding
+ * (channel values in fp32, 22-bit tap quantisation) by 1 / cond: measured |error| ~ 4e-6 / cond on
+ * the [0, 255] scale over the BASELINE configs at full size, i.e. the 1e-3 parity tolerance is
+ * reached near cond = 0.004; the default re-evaluates every pixel below twice that. At most 32768
+ * flagged pixels per call are repaired (the rest keep the fused value); up to 16 calls may be in
+ * flight per device. */
+#define BF_REPAIR_DEFAULT 0.008
 
 BF_API void bf_apply_args_default(bf_apply_args* args);
 
@@ -304,6 +312,13 @@ BF_API bf_status bf_precompute(const bf_plan* plan, int k_count, const void* d_i
                                size_t cache_bytes, bf_stream stream, bf_cache_desc* desc);
 BF_API bf_status bf_apply_cached(const bf_plan* plan, const bf_cache_desc* desc, const void* d_cache,
                                  const void* d_in, float* d_out, bf_stream stream, const bf_apply_args* args);
+
+/* The lowered spatial kernel K~_s(v, u) (eq:Box_N_terms, Appendix A) exactly as the
+ * GPU path applies it (its separable / box-pair / general-pass form), on the integer offsets
+ * u, v in [-r, r]: K[(v + r) * (2r + 1) + (u + r)]; n_values >= (2r + 1)^2 (host memory). For
+ * cross-checking the plan's factorisation against an independent lowering. BF_ERR_UNSUPPORTED if
+ * the plan has no GPU form. */
+BF_API bf_status bf_plan_spatial_kernel(const bf_plan* plan, double* K, size_t n_values);
 
 /* Static string for a status code. */
 BF_API const char* bf_status_string(bf_status s);

@@ -285,9 +285,9 @@ class Plan:
 
 def make_plan(spatial: str, range_kind: str, sigma_s: float, sigma_r: float, radius: int,
               n_terms: int, intensity_max: float = 255.0, n_spatial: int = 9,
-              m_factor: int = 20, **_ignored) -> Plan:
+              m_factor: int = 20, haar_levels: int = 4, **_ignored) -> Plan:
     rng = fit_range(range_kind, sigma_r, intensity_max, n_terms, m_factor)
-    sp = fit_spatial(spatial, sigma_s, radius, n_spatial)
+    sp = fit_spatial(spatial, sigma_s, radius, n_spatial, haar_levels)
     return Plan(rng, sp, float(intensity_max))
 
 

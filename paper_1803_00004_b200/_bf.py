@@ -25,7 +25,7 @@ RANGE = {"gaussian": BF_RANGE_GAUSSIAN, "tukey": BF_RANGE_TUKEY}
 #: every symbol include/bf.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bf_plan_options_default", "bf_plan_create", "bf_plan_destroy", "bf_plan_get_info", "bf_apply",
            "bf_apply_args_default", "bf_apply_ex", "bf_workspace_size", "bf_apply_batched", "bf_apply_config",
-           "bf_apply_host", "bf_apply_launches", "bf_apply_multi", "bf_cache_size", "bf_precompute",
+           "bf_apply_host", "bf_apply_launches", "bf_apply_multi", "bf_cache_size", "bf_precompute", "bf_plan_spatial_kernel",
            "bf_apply_cached", "bf_status_string", "bf_version")
 BF_MAX_PLANS = 4
 
@@ -68,7 +68,7 @@ class PlanInfo(C.Structure):
         ("box_lo_y", C.c_int * BF_MAX_AXIS_BOXES), ("box_hi_y", C.c_int * BF_MAX_AXIS_BOXES),
         ("box_w_y", C.c_double * BF_MAX_AXIS_BOXES),
         ("radius", C.c_int), ("intensity_max", C.c_double), ("input_dtype", C.c_int),
-        ("spatial_rank", C.c_int), ("range_window", C.c_int),
+        ("spatial_rank", C.c_int), ("range_window", C.c_int), ("spatial_passes", C.c_int),
     ]
 
 
@@ -122,6 +122,8 @@ def lib() -> C.CDLL:
         L.bf_precompute.restype = C.c_int
         L.bf_apply_cached.argtypes = [P, C.POINTER(CacheDesc), P, P, P, P, C.POINTER(ApplyArgs)]
         L.bf_apply_cached.restype = C.c_int
+        L.bf_plan_spatial_kernel.argtypes = [P, C.POINTER(C.c_double), C.c_size_t]
+        L.bf_plan_spatial_kernel.restype = C.c_int
         L.bf_status_string.argtypes = [C.c_int]
         L.bf_status_string.restype = C.c_char_p
         L.bf_version.argtypes = []
@@ -173,9 +175,19 @@ class Plan:
             separable=bool(inf.separable),
             boxes_x=[(inf.box_lo_x[i], inf.box_hi_x[i], inf.box_w_x[i]) for i in range(inf.nbx)],
             boxes_y=[(inf.box_lo_y[i], inf.box_hi_y[i], inf.box_w_y[i]) for i in range(inf.nby)],
-            radius=inf.radius, intensity_max=inf.intensity_max, spatial_rank=inf.spatial_rank,
+            radius=inf.radius, intensity_max=inf.intensity_max, spatial_rank=inf.spatial_rank, spatial_passes=inf.spatial_passes,
             range_window="literal" if inf.range_window == 1 else "full",
             input_dtype="u8" if inf.input_dtype == BF_IN_U8 else "f32")
+
+    def spatial_kernel(self):
+        """K~_s(v, u) on the (2r+1)^2 integer offsets as the GPU path applies it (numpy [v+r, u+r])."""
+        import numpy as np
+        r = self.info()["radius"]
+        n = 2 * r + 1
+        K = np.zeros((n, n), dtype=np.float64)
+        _check(lib().bf_plan_spatial_kernel(self._h, K.ctypes.data_as(C.POINTER(C.c_double)), K.size),
+               "bf_plan_spatial_kernel")
+        return K
 
     def close(self) -> None:
         if getattr(self, "_h", None):

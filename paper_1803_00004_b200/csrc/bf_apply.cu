@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "bf_params.h"
 
@@ -175,6 +176,7 @@ void quantise(const bf_plan* p, KParams& P) {
       P.ax[t][b] = (int)std::lround(std::ldexp(p->swx[t][b] / wxmax, abits));
     }
   }
+  P.uscale = std::ldexp(wxmax * wymax, -(qb - P.ush + abits - 32));
   const double invD = 1.0 / p->D;
   P.invD = invD;
   P.invD_hi = (float)invD;
@@ -236,27 +238,51 @@ void repair_params(const bf_plan* const* plans, int nplans, int n_frames, int H,
   R.D = p->D;
   R.T = p->T;
   R.u8 = p->input_dtype == BF_IN_U8;
-  R.ns = p->ns;
+  // spatial terms: the box-pair form (ns <= 2) or the general plan's separable passes
+  R.ns = p->ns > 0 ? p->ns : p->n_pass;
   int rad = 0;
-  for (int s = 0; s < p->ns; ++s) {
-    R.nbx[s] = p->snbx[s];
-    R.nby[s] = p->snby[s];
-    for (int b = 0; b < p->snbx[s]; ++b) {
-      R.lox[s][b] = p->slox[s][b];
-      R.hix[s][b] = p->shix[s][b];
-      R.wx[s][b] = p->swx[s][b];
+  for (int s = 0; s < R.ns; ++s) {
+    const bool gen = p->ns == 0;
+    R.nbx[s] = gen ? p->pass[s].nbx : p->snbx[s];
+    R.nby[s] = gen ? p->pass[s].nby : p->snby[s];
+    for (int b = 0; b < R.nbx[s]; ++b) {
+      R.lox[s][b] = gen ? p->pass[s].lox[b] : p->slox[s][b];
+      R.hix[s][b] = gen ? p->pass[s].hix[b] : p->shix[s][b];
+      R.wx[s][b] = gen ? p->pass[s].wx[b] : p->swx[s][b];
       rad = std::max(rad, std::max(-R.lox[s][b], R.hix[s][b]));
     }
-    for (int b = 0; b < p->snby[s]; ++b) {
-      R.loy[s][b] = p->sloy[s][b];
-      R.hiy[s][b] = p->shiy[s][b];
-      R.wy[s][b] = p->swy[s][b];
+    for (int b = 0; b < R.nby[s]; ++b) {
+      R.loy[s][b] = gen ? p->pass[s].loy[b] : p->sloy[s][b];
+      R.hiy[s][b] = gen ? p->pass[s].hiy[b] : p->shiy[s][b];
+      R.wy[s][b] = gen ? p->pass[s].wy[b] : p->swy[s][b];
       rad = std::max(rad, std::max(-R.loy[s][b], R.hiy[s][b]));
     }
   }
   R.rad = rad;
+  // chunks of window rows per pixel (~16 K taps each: a few hundred pixels fill the GPU, one
+  // pixel's latency stays short); partial sums are added in fixed point: each chunk's |den| is
+  // at most sum_s sum_b |wx| |wy| (box areas) * sum_k |a_k| over the whole window
+  const int n1 = 2 * rad + 1;
+  R.nch = std::max(1, std::min(64, (int)(((long long)n1 * n1 + 16383) / 16384)));
+  R.rpc = (n1 + R.nch - 1) / R.nch;
+  R.nch = (n1 + R.rpc - 1) / R.rpc;
+  double sabs = 0.0;
+  for (int s = 0; s < R.ns; ++s) {
+    double fx = 0.0, fy = 0.0;
+    for (int b = 0; b < R.nbx[s]; ++b) fx += std::fabs(R.wx[s][b]) * (R.hix[s][b] - R.lox[s][b] + 1);
+    for (int b = 0; b < R.nby[s]; ++b) fy += std::fabs(R.wy[s][b]) * (R.hiy[s][b] - R.loy[s][b] + 1);
+    sabs += fx * fy;
+  }
+  double amax = 0.0;
+  for (int q = 0; q < nplans; ++q) {
+    double as = 0.0;
+    for (int i = 0; i < plans[q]->n_k; ++i) as += std::fabs(plans[q]->a[i]);
+    amax = std::max(amax, as);
+  }
+  R.qscale = std::ldexp(1.0, 61) / std::max(1e-300, sabs * amax * std::max(1.0, p->D));
   R.count = S.count;
   R.list = S.list;
+  R.acc = S.acc;
   R.cap = S.cap;
   R.fb_count = A.d_fallback_count;
   R.fb_mask = A.d_fallback_mask;
@@ -269,7 +295,7 @@ bf_status repair_sink(const bf_apply_args& A, double wscale, double mfull, cudaS
   if (A.repair_threshold < 0) return BF_OK;
   const double tau = A.repair_threshold > 0 ? A.repair_threshold : BF_REPAIR_DEFAULT;
   const unsigned slot = g_repair_ticket.fetch_add(1, std::memory_order_relaxed) % REPAIR_SLOTS;
-  if (repair_slot(slot, &S.count, &S.list) != cudaSuccess) return BF_ERR_CUDA;
+  if (repair_slot(slot, &S.count, &S.list, &S.acc) != cudaSuccess) return BF_ERR_CUDA;
   if (cudaMemsetAsync(S.count, 0, sizeof(unsigned), st) != cudaSuccess) return BF_ERR_CUDA;
   S.cap = REPAIR_CAP;
   S.tau_w = tau * wscale;
@@ -315,7 +341,7 @@ size_t smem_ws2(int cols, int nkc, int tw, int G, bool u8, int& l_off, int& r_of
   l_off = (int)off;
   if (u8) off += 256 * (sizeof(float2) + sizeof(double2));
   r_off = (int)off;
-  if (G > 1) off += 2 * (size_t)(G - 1) * tw * sizeof(longlong2);
+  if (G > 1) off += 2 * (size_t)tw * 2 * sizeof(longlong2);   // per row parity: sum of the senders' (num_b, den_b)
   return off;
 }
 
@@ -562,6 +588,85 @@ cudaError_t dispatch(const LaunchSpec& s, const KParams& P, const void* in, floa
   return launch_band(s, P, in, out, ws, grid, smem, st);
 }
 
+// The launches of one prepared plan: kernel 2b runs every term in one launch (split over its
+// cluster), kernels 1 / 2 one launch per MAXK terms. gl counts launches across the calls of one
+// apply; gtotal >= 0 (general plans: fp64 workspace passes over several spatial passes) makes the
+// pass code follow the global launch index, else the plan's own term passes.
+cudaError_t enqueue(const Req& R, const bf_plan* p, Launch& L, int wbits, const void* d_in, float* d_out,
+                    longlong2* ws, cudaStream_t st, int& gl, int gtotal) {
+  const bool dump = R.dump;
+  auto code = [&](int local, int nlocal) {
+    if (gtotal < 0) return (nlocal == 1) ? 0 : (local == 0 ? 1 : (local == nlocal - 1 ? 3 : 2));
+    return (gtotal == 1) ? 0 : (gl == 0 ? 1 : (gl == gtotal - 1 ? 3 : 2));
+  };
+  cudaError_t err = cudaSuccess;
+  if (L.spec.kern == KERN_WS2 && !dump) {   // one launch, every term (split over the cluster)
+    set_terms(R, p, 0, p->n_k, wbits, L.P);
+    L.P.pass = code(0, 1);
+    err = dispatch(L.spec, L.P, d_in, d_out, ws, L.grid, L.smem, st);
+    ++gl;
+    return err;
+  }
+  const int per = dump ? 16 : L.spec.MAXK;
+  for (int pass = 0; pass < L.passes && err == cudaSuccess; ++pass) {
+    const int first = pass * per;
+    const int nk = std::min(per, p->n_k - first);
+    set_terms(R, p, first, nk, wbits, L.P);
+    L.P.ngrp = (4 * nk + 31) / 32;
+    LaunchSpec sp = L.spec;
+    sp.FULL = (nk == sp.MAXK);
+    if (sp.NPL > 1) sp.FULL = false;
+    for (int i = 1; i < nk; ++i)
+      if (L.P.kval[i] != L.P.kval[i - 1] + 1) sp.CONSEC = false;
+    if (dump) {
+      L.P.pass = 0;
+    } else {
+      L.P.pass = code(pass, L.passes);
+      // walker segments (kernel 1): ngrp * nseg warps; long segments amortise the window sums
+      if (sp.kern == KERN_BAND) {
+        const int max_tasks = sp.NT / 32;
+        const int halo = L.P.TW >= 0 ? (sp.NT - L.P.TW) : 0;
+        int nseg = std::max(1, max_tasks / L.P.ngrp);
+        const int min_len = std::max(32, 2 * (halo + 1) / 3);
+        while (nseg > 1 && (L.P.TW + nseg - 1) / nseg < min_len) --nseg;
+        // wide halos (NT = 512): four segments measured best on cfg4 (r = 192)
+        if (sp.NT == 512) nseg = std::min(4, std::max(1, max_tasks / L.P.ngrp));
+        L.P.nseg = nseg;
+        L.P.seglen = (L.P.TW + nseg - 1) / nseg;
+        L.P.seglen += L.P.seglen & 1;
+      } else if (sp.kern == KERN_WS) {   // F warps: (WS_F / 32) / ngrp segments per group
+        L.P.nseg = std::max(1, (WS_F / 32) / L.P.ngrp);
+        L.P.seglen = (L.P.TW + L.P.nseg - 1) / L.P.nseg;
+        L.P.seglen += L.P.seglen & 1;
+      }
+    }
+    err = dispatch(sp, L.P, d_in, d_out, ws, L.grid, L.smem, st);
+    ++gl;
+  }
+  return err;
+}
+
+// Spatial pass q of a general plan as a separable plan (ns = 1) with the same range terms.
+void pass_plan(const bf_plan* p, int q, bf_plan& t) {
+  t = *p;
+  const auto& P = p->pass[q];
+  t.ns = 1;
+  t.separable = 1;
+  t.n_pass = 0;
+  t.snbx[0] = t.nbx = P.nbx;
+  t.snby[0] = t.nby = P.nby;
+  for (int b = 0; b < P.nbx; ++b) {
+    t.slox[0][b] = t.lox[b] = P.lox[b];
+    t.shix[0][b] = t.hix[b] = P.hix[b];
+    t.swx[0][b] = t.wx[b] = P.wx[b];
+  }
+  for (int b = 0; b < P.nby; ++b) {
+    t.sloy[0][b] = t.loy[b] = P.loy[b];
+    t.shiy[0][b] = t.hiy[b] = P.hiy[b];
+    t.swy[0][b] = t.wy[b] = P.wy[b];
+  }
+}
+
 // ---- the literal-window path (kernel 3): u8 input, levels 0..255 (D = 255), separable plans with
 // at most two boxes per axis whose halo fits the 128-column strip.
 bf_status literal_launch(const bf_plan* p, int n_frames, int H, int W, LParams& Lp, dim3& grid, size_t& smem) {
@@ -629,6 +734,61 @@ bf_status literal_launch(const bf_plan* p, int n_frames, int H, int W, LParams& 
   return BF_OK;
 }
 
+// General spatial plan (NEXT f3): one separable pass per box product (the plan's exact rank
+// factorisation), num / den summed in absolute units in the fp64 workspace; the last launch divides.
+bf_status run_general(const Req& R, const bf_plan* const* plans, int nplans, const bf_plan* p, const void* d_in,
+                      float* d_out, int n_frames, int H, int W, cudaStream_t st, const bf_apply_args& A,
+                      bf_launch_config* dry) {
+  if (nplans != 1 || R.dump || p->n_pass < 1) return BF_ERR_UNSUPPORTED;
+  std::vector<Launch> Ls(p->n_pass);
+  bf_plan tq;
+  int total = 0;
+  for (int q = 0; q < p->n_pass; ++q) {
+    pass_plan(p, q, tq);
+    const bf_status sq = prepare(R, &tq, Ls[q]);
+    if (sq != BF_OK) return sq;
+    total += (Ls[q].spec.kern == KERN_WS2) ? 1 : Ls[q].passes;
+  }
+  const size_t wsb = sizeof(double2) * (size_t)H * W * n_frames;
+  if (dry) {
+    const Launch& L0 = Ls[0];
+    *dry = bf_launch_config{total, L0.name, L0.threads, (int)L0.grid.x, (int)L0.grid.y, (int)L0.grid.z, L0.P.TW,
+                            L0.P.TH, L0.smem, L0.P.G, L0.spec.kern == KERN_WS2 ? L0.P.tpc : L0.spec.MAXK,
+                            L0.spec.COLS, wsb};
+    return BF_OK;
+  }
+  if (!A.d_workspace || A.workspace_bytes < wsb) return BF_ERR_WORKSPACE;
+  longlong2* ws = static_cast<longlong2*>(A.d_workspace);
+  const int wbits = combine_bits(plans, nplans);
+  double mass_abs = 0.0;   // sum of K~_s over the whole window (absolute units)
+  for (int q = 0; q < p->n_pass; ++q) {
+    double fx = 0.0, fy = 0.0;
+    for (int b = 0; b < p->pass[q].nbx; ++b) fx += p->pass[q].wx[b] * (p->pass[q].hix[b] - p->pass[q].lox[b] + 1);
+    for (int b = 0; b < p->pass[q].nby; ++b) fy += p->pass[q].wy[b] * (p->pass[q].hiy[b] - p->pass[q].loy[b] + 1);
+    mass_abs += fx * fy;
+  }
+  RepairSink S;
+  const bf_status rs = repair_sink(A, 1.0, mass_abs, st, S);
+  if (rs != BF_OK) return rs;
+  int gl = 0;
+  cudaError_t err = cudaSuccess;
+  for (int q = 0; q < p->n_pass && err == cudaSuccess; ++q) {
+    pass_plan(p, q, tq);
+    Launch& L = Ls[q];
+    L.P.fb_count = A.d_fallback_count;
+    L.P.fb_mask = A.d_fallback_mask;
+    L.P.rep = S;
+    L.P.dunit = std::ldexp(L.P.uscale, -wbits);
+    err = enqueue(R, &tq, L, wbits, d_in, d_out, ws, st, gl, total);
+  }
+  if (err == cudaSuccess && S.count) {
+    RParams Rp;
+    repair_params(plans, nplans, n_frames, H, W, A, S, Rp);
+    err = launch_repair(Rp, d_in, d_out, st);
+  }
+  return err == cudaSuccess ? BF_OK : BF_ERR_CUDA;
+}
+
 // One call: validation, launch shape, and (unless dry) the launches.
 bf_status run(const bf_plan* const* plans, int nplans, const void* d_in, float* d_out, int n_frames, int H, int W,
               cudaStream_t st, const bf_apply_args* args, bf_launch_config* dry, bool dump = false) {
@@ -688,8 +848,13 @@ bf_status run(const bf_plan* const* plans, int nplans, const void* d_in, float* 
   }
   if (A.u8_trig != 0 && A.u8_trig != 1) return BF_ERR_INVALID_ARG;
   Req R{plans, nplans, n_frames, H, W, ya, yb, A.kernel, A.band_rows, dump, A.u8_trig == 1};
+  if (p->ns == 0 && p->n_pass > 0) return run_general(R, plans, nplans, p, d_in, d_out, n_frames, H, W, st, A, dry);
+
   Launch L;
   const bf_status s = prepare(R, p, L);
+  // rank-2 plans the box-pair kernel cannot run (e.g. radii above its strip): two separable passes
+  if (s == BF_ERR_UNSUPPORTED && p->ns == 2 && p->n_pass == 2 && nplans == 1 && !dump)
+    return run_general(R, plans, nplans, p, d_in, d_out, n_frames, H, W, st, A, dry);
   if (s != BF_OK) return s;
   if (dry) {
     *dry = bf_launch_config{L.passes, L.name, L.threads, (int)L.grid.x, (int)L.grid.y, (int)L.grid.z, L.P.TW,
@@ -709,48 +874,8 @@ bf_status run(const bf_plan* const* plans, int nplans, const void* d_in, float* 
     const bf_status rs = repair_sink(A, std::ldexp(1.0, wbits), mass_full(p, L.P), st, L.P.rep);
     if (rs != BF_OK) return rs;
   }
-  cudaError_t err = cudaSuccess;
-  if (L.spec.kern == KERN_WS2 && !dump) {   // one launch, every term (split over the cluster)
-    set_terms(R, p, 0, p->n_k, wbits, L.P);
-    L.P.pass = 0;
-    err = dispatch(L.spec, L.P, d_in, d_out, ws, L.grid, L.smem, st);
-  } else {
-    const int per = dump ? 16 : L.spec.MAXK;
-    for (int pass = 0; pass < L.passes && err == cudaSuccess; ++pass) {
-      const int first = pass * per;
-      const int nk = std::min(per, p->n_k - first);
-      set_terms(R, p, first, nk, wbits, L.P);
-      L.P.ngrp = (4 * nk + 31) / 32;
-      LaunchSpec sp = L.spec;
-      sp.FULL = (nk == sp.MAXK);
-      if (sp.NPL > 1) sp.FULL = false;
-      for (int i = 1; i < nk; ++i)
-        if (L.P.kval[i] != L.P.kval[i - 1] + 1) sp.CONSEC = false;
-      if (dump) {
-        L.P.pass = 0;
-      } else {
-        L.P.pass = (L.passes == 1) ? 0 : (pass == 0 ? 1 : (pass == L.passes - 1 ? 3 : 2));
-        // walker segments (kernel 1): ngrp * nseg warps; long segments amortise the window sums
-        if (sp.kern == KERN_BAND) {
-          const int max_tasks = sp.NT / 32;
-          const int halo = L.P.TW >= 0 ? (sp.NT - L.P.TW) : 0;
-          int nseg = std::max(1, max_tasks / L.P.ngrp);
-          const int min_len = std::max(32, 2 * (halo + 1) / 3);
-          while (nseg > 1 && (L.P.TW + nseg - 1) / nseg < min_len) --nseg;
-          // wide halos (NT = 512): four segments measured best on cfg4 (r = 192)
-          if (sp.NT == 512) nseg = std::min(4, std::max(1, max_tasks / L.P.ngrp));
-          L.P.nseg = nseg;
-          L.P.seglen = (L.P.TW + nseg - 1) / nseg;
-          L.P.seglen += L.P.seglen & 1;
-        } else if (sp.kern == KERN_WS) {   // F warps: (WS_F / 32) / ngrp segments per group
-          L.P.nseg = std::max(1, (WS_F / 32) / L.P.ngrp);
-          L.P.seglen = (L.P.TW + L.P.nseg - 1) / L.P.nseg;
-          L.P.seglen += L.P.seglen & 1;
-        }
-      }
-      err = dispatch(sp, L.P, d_in, d_out, ws, L.grid, L.smem, st);
-    }
-  }
+  int gl = 0;
+  cudaError_t err = enqueue(R, p, L, wbits, d_in, d_out, ws, st, gl, -1);
   if (err == cudaSuccess && L.P.rep.count) {
     RParams Rp;
     repair_params(plans, nplans, n_frames, H, W, A, L.P.rep, Rp);

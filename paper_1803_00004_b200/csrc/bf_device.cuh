@@ -469,12 +469,14 @@ __device__ __forceinline__ void note_fallback(unsigned long long* cnt, unsigned 
   }
 }
 
-// Appends the pixel to the repair list when den < tau mass (RepairSink). Returns true if flagged
-// (its fallback bookkeeping is then the repair pass's).
-__device__ __forceinline__ bool flag_pixel(const RepairSink& R, long long den, int mass, long long pix) {
+// Appends the pixel to the repair list when den < tau mass (RepairSink): den and mass in the same
+// units (mass = the k = 0 cosine channel's box sum; mass_full scaled by mass_unit when that channel
+// is not at hand). Returns true if flagged (its fallback bookkeeping is then the repair pass's).
+__device__ __forceinline__ bool flag_pixel(const RepairSink& R, double den, double mass, double mass_unit,
+                                           long long pix) {
   if (!R.count) return false;
-  const double m = mass > 0 ? (double)mass : R.mass_full;
-  const bool fl = (double)den < R.tau_w * m;
+  const double m = mass > 0 ? mass : R.mass_full * mass_unit;
+  const bool fl = den < R.tau_w * m;
   const unsigned act = __activemask();
   const unsigned bal = __ballot_sync(act, fl);
   if (bal) {
@@ -484,10 +486,38 @@ __device__ __forceinline__ bool flag_pixel(const RepairSink& R, long long den, i
     base = __shfl_sync(act, base, leader);
     if (fl) {
       const unsigned i = base + __popc(bal & ((1u << lane) - 1));
-      if (i < R.cap) R.list[i] = (unsigned long long)pix;
+      if (i < R.cap) {
+        R.list[i] = (unsigned long long)pix;
+        R.acc[i] = RepAcc{0, 0, 0u, 0u};
+      }
     }
   }
   return fl;
+}
+__device__ __forceinline__ bool flag_pixel(const RepairSink& R, long long den, int mass, long long pix) {
+  return flag_pixel(R, (double)den, (double)mass, 1.0, pix);
+}
+
+// General plans (several separable passes, P.dunit != 0): the launch's num / den, converted to
+// absolute units (n with the factor D of the I channels), go to / from the fp64 workspace; the last
+// launch divides. The repair flag then compares den with tau times the unclipped spatial mass in
+// the same units (rep.tau_w = tau, rep.mass_full = sum K~_s).
+__device__ __forceinline__ void finish_dws(const KParams& P, double n, double d, float Ic, long long pix,
+                                           float* __restrict__ out, void* ws) {
+  double2* w = static_cast<double2*>(ws);
+  if (P.pass >= 2) {
+    const double2 a = w[pix];
+    n += a.x;
+    d += a.y;
+  }
+  if (P.pass == 1 || P.pass == 2) {
+    w[pix] = make_double2(n, d);
+    return;
+  }
+  const bool fb = !(d > 0);
+  out[pix] = fb ? Ic : (float)(n / d);
+  const bool fl = flag_pixel(P.rep, d, 0.0, 1.0, pix);
+  note_fallback(P.fb_count, P.fb_mask, pix, fb && !fl);
 }
 
 // out = D num / den (den <= 0: I(x), Q18), or the int64 pair to / from the multi-pass workspace;
@@ -495,6 +525,10 @@ __device__ __forceinline__ bool flag_pixel(const RepairSink& R, long long den, i
 __device__ __forceinline__ void finish_pixel(const KParams& P, long long num, long long den, float Ic, long long pix,
                                              float* __restrict__ out, longlong2* __restrict__ ws, bool count = true,
                                              int mass = 0) {
+  if (P.dunit != 0.0) {
+    finish_dws(P, (double)num * P.dunit * P.D, (double)den * P.dunit, Ic, pix, out, ws);
+    return;
+  }
   if (P.pass == 1) {
     ws[pix] = make_longlong2(num, den);
     return;
@@ -512,6 +546,26 @@ __device__ __forceinline__ void finish_pixel(const KParams& P, long long num, lo
   out[pix] = fb ? Ic : (float)(P.D * (double)num / (double)den);
   const bool fl = flag_pixel(P.rep, den, mass, pix);
   if (count) note_fallback(P.fb_count, P.fb_mask, pix, fb && !fl);
+}
+
+// Kernel 2b's finish from the per-box accumulators num_b = sum W H_b, den_b (exact int64):
+// num = sum_b ax_b num_b, den likewise, formed in fp64 (relative rounding 2^-53, far below the
+// channel values' fp32 error); out = D num / den, or I(x) if den <= 0 (Q18). mass is in the same
+// units (sum_b ax_b H_b of the k = 0 cosine channel, 2^32 times the F units of finish_pixel).
+__device__ __forceinline__ void finish_pixel_pb(const KParams& P, const long long (&num)[2], const long long (&den)[2],
+                                                int ax0, int ax1, float Ic, long long pix, float* __restrict__ out,
+                                                double mass, void* ws) {
+  const double n = fma((double)num[1], (double)ax1, (double)num[0] * (double)ax0);
+  const double d = fma((double)den[1], (double)ax1, (double)den[0] * (double)ax0);
+  if (P.dunit != 0.0) {
+    const double u = P.dunit * 2.3283064365386963e-10;   // / 2^32: F units
+    finish_dws(P, n * u * P.D, d * u, Ic, pix, out, ws);
+    return;
+  }
+  const bool fb = !(d > 0);
+  out[pix] = fb ? Ic : (float)(P.D * n / d);
+  const bool fl = flag_pixel(P.rep, d, mass, 4294967296.0, pix);
+  note_fallback(P.fb_count, P.fb_mask, pix, fb && !fl);
 }
 
 template <bool U8>

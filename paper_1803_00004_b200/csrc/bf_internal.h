@@ -4,6 +4,7 @@
 #include "../../include/bf.h"
 
 #define BF_MAX_RADIUS 1024
+#define BF_MAX_SP_PASSES 32
 
 struct bf_plan {
   int ks, kr;
@@ -39,4 +40,17 @@ struct bf_plan {
   double swx[2][BF_MAX_AXIS_BOXES];
   int snby[2], sloy[2][BF_MAX_AXIS_BOXES], shiy[2][BF_MAX_AXIS_BOXES];
   double swy[2][BF_MAX_AXIS_BOXES];
+  // general plans (NEXT f3: no separable / rank-2 form, e.g. N_s = 13, 25 at J = 4): K~_s as a sum
+  // of n_pass separable box products (an exact rank factorisation of the kernel's box-weight matrix,
+  // each factor's boxes cut into groups of at most BF_MAX_AXIS_BOXES); the GPU runs one separable
+  // pass per product and accumulates num / den in fp64 (ns = 0 then).
+  int n_pass;
+  int rank;
+  struct {
+    int nbx, nby;
+    int lox[BF_MAX_AXIS_BOXES], hix[BF_MAX_AXIS_BOXES];
+    double wx[BF_MAX_AXIS_BOXES];
+    int loy[BF_MAX_AXIS_BOXES], hiy[BF_MAX_AXIS_BOXES];
+    double wy[BF_MAX_AXIS_BOXES];
+  } pass[BF_MAX_SP_PASSES];
 };

@@ -17,9 +17,17 @@ constexpr int MAXP = BF_MAX_PLANS;   // range plans of one bf_apply_multi
 // den <= 0, whose fallback decision rides on that rounding) is appended to a device list and
 // re-evaluated by bf_repair_kernel in fp64 straight from the approximated kernels (the direct
 // double loop of pin P1, equal to the box evaluation up to rounding).
+// Per flagged pixel: the repair pass's fixed-point accumulators (zeroed by the flagging kernel)
+struct RepAcc {
+  long long num, den;   // sum of the chunks' partial sums, each rounded to fixed point (exact adds)
+  unsigned arrived;     // chunks done
+  unsigned pad;
+};
+
 struct RepairSink {
   unsigned* count;            // list length (atomic), NULL = repair off
   unsigned long long* list;   // output indices (frame and plan offsets included)
+  RepAcc* acc;                // per list entry
   unsigned cap;
   double tau_w;               // tau * 2^wbits: flag if den < tau_w * mass (mass = the k = 0 cosine channel F)
   double mass_full;           // that channel's value for an unclipped window (used when k = 0 is not selected)
@@ -61,6 +69,8 @@ struct KParams {
   int* cache;                 // bf_precompute: box-filtered channel planes F[ch][y][x] (int32)
   long long cache_plane;      // elements per cache plane (H * W)
   RepairSink rep;             // ill-conditioned pixels for the fp64 repair pass
+  double uscale;              // absolute value of one unit of F (times 2^wbits): wxmax wymax 2^-(abits-32+q-ush)
+  double dunit;               // general plans: uscale * 2^-wbits, num / den accumulated in fp64 (0 = off)
 };
 
 // Template choices of one launch (the kernel TUs switch on these).
@@ -150,20 +160,23 @@ struct RParams {
   double D, T;                // cosine period half-width T (= D on the hot path)
   int u8;
   int ns;                     // spatial box-pair terms K~_s(u, v) = sum_s fx_s(u) fy_s(v)
-  int nbx[2], nby[2];
-  int lox[2][MAXB], hix[2][MAXB], loy[2][MAXB], hiy[2][MAXB];
-  double wx[2][MAXB], wy[2][MAXB];
+  int nbx[BF_MAX_SP_PASSES], nby[BF_MAX_SP_PASSES];
+  int lox[BF_MAX_SP_PASSES][MAXB], hix[BF_MAX_SP_PASSES][MAXB], loy[BF_MAX_SP_PASSES][MAXB], hiy[BF_MAX_SP_PASSES][MAXB];
+  double wx[BF_MAX_SP_PASSES][MAXB], wy[BF_MAX_SP_PASSES][MAXB];
   int rad;                    // window half-width (max box extent)
+  int nch, rpc;               // chunks per pixel, window rows per chunk
+  double qscale;              // fixed-point scale of the partial sums: |den partial| * qscale < 2^61
   unsigned* count;
   const unsigned long long* list;
+  RepAcc* acc;
   unsigned cap;
   unsigned long long* fb_count;
   unsigned char* fb_mask;
   unsigned long long* repaired;   // optional: += pixels re-evaluated
 };
-constexpr unsigned REPAIR_SLOTS = 16, REPAIR_CAP = 1u << 16;
-// device addresses of repair slot s's counter and list (static device storage of the library)
-cudaError_t repair_slot(unsigned s, unsigned** count, unsigned long long** list);
+constexpr unsigned REPAIR_SLOTS = 16, REPAIR_CAP = 1u << 15;
+// device addresses of repair slot s's counter, list and accumulators (static device storage)
+cudaError_t repair_slot(unsigned s, unsigned** count, unsigned long long** list, RepAcc** acc);
 cudaError_t launch_repair(const RParams& R, const void* in, float* out, cudaStream_t st);
 
 }  // namespace bf

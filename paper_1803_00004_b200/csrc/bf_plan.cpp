@@ -293,6 +293,146 @@ bool box_pair_rank2(const std::vector<double>& K, int r, bf_plan* p) {
   return true;
 }
 
+// Any step function on offsets -r..r as boxes sum_i w_i [lo_i, hi_i] (no count limit): nested
+// symmetric boxes when f is even, else its constant pieces.
+void step_boxes(const std::vector<double>& f, int r, std::vector<int>& lo, std::vector<int>& hi,
+                std::vector<double>& w) {
+  const int n = 2 * r + 1;
+  double fmax = 0.0;
+  for (double v : f) fmax = std::max(fmax, std::fabs(v));
+  const double tol = 1e-13 * (fmax > 0 ? fmax : 1.0);
+  bool sym = true;
+  for (int i = 0; i < n; ++i)
+    if (std::fabs(f[i] - f[n - 1 - i]) > tol) sym = false;
+  lo.clear();
+  hi.clear();
+  w.clear();
+  if (sym) {
+    double prev = 0.0;
+    for (int e = r; e >= 0; --e) {
+      const double v = f[e + r];
+      if (std::fabs(v - prev) > tol) {
+        lo.push_back(-e);
+        hi.push_back(e);
+        w.push_back(v - prev);
+        prev = v;
+      }
+    }
+    return;
+  }
+  int start = 0;
+  for (int i = 1; i <= n; ++i)
+    if (i == n || std::fabs(f[i] - f[start]) > tol) {
+      if (std::fabs(f[start]) > tol) {
+        lo.push_back(start - r);
+        hi.push_back(i - 1 - r);
+        w.push_back(f[start]);
+      }
+      start = i;
+    }
+}
+
+// General plans: K (n x n, [v][u]) is piecewise constant on a grid of cells (the Haar terms'
+// breakpoints); its cell matrix C (rows: y cells, columns: x cells) is factored exactly as
+// C = sum_s col_s row_s^T by Gaussian elimination with full pivoting (rank R <= min cells), so
+// K~_s(v, u) = sum_s fx_s(u) fy_s(v) with step functions fx_s, fy_s; each becomes boxes
+// (step_boxes) cut into groups of at most BF_MAX_AXIS_BOXES, one separable pass per pair of
+// groups. Checked on every offset against K. Returns false if it needs more than
+// BF_MAX_SP_PASSES passes.
+bool general_passes(const std::vector<double>& K, int r, bf_plan* p) {
+  const int n = 2 * r + 1;
+  double kmax = 0.0;
+  for (double v : K) kmax = std::max(kmax, std::fabs(v));
+  if (kmax == 0.0) return false;
+  const double tol = 1e-13 * kmax;
+  std::vector<int> cx{0}, cy{0};   // first offset index of every cell
+  for (int u = 1; u < n; ++u) {
+    bool d = false;
+    for (int v = 0; v < n && !d; ++v) d = std::fabs(K[(size_t)v * n + u] - K[(size_t)v * n + u - 1]) > tol;
+    if (d) cx.push_back(u);
+  }
+  for (int v = 1; v < n; ++v) {
+    bool d = false;
+    for (int u = 0; u < n && !d; ++u) d = std::fabs(K[(size_t)v * n + u] - K[(size_t)(v - 1) * n + u]) > tol;
+    if (d) cy.push_back(v);
+  }
+  const int nx = (int)cx.size(), ny = (int)cy.size();
+  std::vector<double> C((size_t)ny * nx);
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i) C[(size_t)j * nx + i] = K[(size_t)cy[j] * n + cx[i]];
+  std::vector<std::vector<double>> cols, rows;   // per rank term: y-cell values, x-cell values
+  for (int it = 0; it < std::min(nx, ny); ++it) {
+    int bj = 0, bi = 0;
+    double best = 0.0;
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i)
+        if (std::fabs(C[(size_t)j * nx + i]) > best) {
+          best = std::fabs(C[(size_t)j * nx + i]);
+          bj = j;
+          bi = i;
+        }
+    if (best <= 1e-12 * kmax) break;
+    const double piv = C[(size_t)bj * nx + bi];
+    std::vector<double> col(ny), row(nx);
+    for (int j = 0; j < ny; ++j) col[j] = C[(size_t)j * nx + bi];
+    for (int i = 0; i < nx; ++i) row[i] = C[(size_t)bj * nx + i] / piv;
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) C[(size_t)j * nx + i] -= col[j] * row[i];
+    cols.push_back(col);
+    rows.push_back(row);
+  }
+  p->rank = (int)cols.size();
+  p->n_pass = 0;
+  for (int s = 0; s < p->rank; ++s) {
+    std::vector<double> fx(n), fy(n);
+    for (int i = 0, c = 0; i < n; ++i) {
+      while (c + 1 < nx && cx[c + 1] <= i) ++c;
+      fx[i] = rows[s][c];
+    }
+    for (int i = 0, c = 0; i < n; ++i) {
+      while (c + 1 < ny && cy[c + 1] <= i) ++c;
+      fy[i] = cols[s][c];
+    }
+    std::vector<int> lx, hx, ly, hy;
+    std::vector<double> wx, wy;
+    step_boxes(fx, r, lx, hx, wx);
+    step_boxes(fy, r, ly, hy, wy);
+    for (size_t gx = 0; gx < lx.size(); gx += BF_MAX_AXIS_BOXES)
+      for (size_t gy = 0; gy < ly.size(); gy += BF_MAX_AXIS_BOXES) {
+        if (p->n_pass >= BF_MAX_SP_PASSES) return false;
+        auto& P = p->pass[p->n_pass++];
+        P.nbx = (int)std::min<size_t>(BF_MAX_AXIS_BOXES, lx.size() - gx);
+        P.nby = (int)std::min<size_t>(BF_MAX_AXIS_BOXES, ly.size() - gy);
+        for (int b = 0; b < P.nbx; ++b) {
+          P.lox[b] = lx[gx + b];
+          P.hix[b] = hx[gx + b];
+          P.wx[b] = wx[gx + b];
+        }
+        for (int b = 0; b < P.nby; ++b) {
+          P.loy[b] = ly[gy + b];
+          P.hiy[b] = hy[gy + b];
+          P.wy[b] = wy[gy + b];
+        }
+      }
+  }
+  // exact check on every offset
+  for (int v = 0; v < n; ++v)
+    for (int u = 0; u < n; ++u) {
+      double k = 0.0;
+      for (int q = 0; q < p->n_pass; ++q) {
+        const auto& P = p->pass[q];
+        double a = 0.0, b = 0.0;
+        for (int i = 0; i < P.nbx; ++i)
+          if (u - r >= P.lox[i] && u - r <= P.hix[i]) a += P.wx[i];
+        for (int i = 0; i < P.nby; ++i)
+          if (v - r >= P.loy[i] && v - r <= P.hiy[i]) b += P.wy[i];
+        k += a * b;
+      }
+      if (std::fabs(k - K[(size_t)v * n + u]) > 1e-10 * kmax) return false;
+    }
+  return p->n_pass > 0;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ public entry points
@@ -461,8 +601,30 @@ extern "C" bf_status bf_plan_create(bf_plan** out, int ks, int kr, double sigma_
         p->shiy[0][b] = p->hiy[b];
         p->swy[0][b] = p->wy[b];
       }
-    } else if (!box_pair_rank2(K, radius, p)) {
-      p->ns = 0;   // no GPU form: bf_apply returns BF_ERR_UNSUPPORTED
+    } else if (box_pair_rank2(K, radius, p)) {
+      // the same two terms as separable passes, for radii the rank-2 kernel cannot run
+      p->rank = 2;
+      p->n_pass = 2;
+      for (int s = 0; s < 2; ++s) {
+        auto& P = p->pass[s];
+        P.nbx = p->snbx[s];
+        P.nby = p->snby[s];
+        for (int b = 0; b < P.nbx; ++b) {
+          P.lox[b] = p->slox[s][b];
+          P.hix[b] = p->shix[s][b];
+          P.wx[b] = p->swx[s][b];
+        }
+        for (int b = 0; b < P.nby; ++b) {
+          P.loy[b] = p->sloy[s][b];
+          P.hiy[b] = p->shiy[s][b];
+          P.wy[b] = p->swy[s][b];
+        }
+      }
+    } else {
+      p->ns = 0;
+      // no GPU form -> bf_apply returns BF_ERR_UNSUPPORTED (also when the repair pass's fp64 factor
+      // tables, 2 x passes x (2r + 1) doubles, would not fit its shared memory)
+      if (!general_passes(K, radius, p) || p->n_pass * (2 * radius + 1) > 12288) p->n_pass = 0;
     }
   }
   *out = p;
@@ -494,7 +656,8 @@ extern "C" bf_status bf_plan_get_info(const bf_plan* p, bf_plan_info* info) {
     info->sp_coef[i] = p->sp_coef[i];
   }
   info->separable = p->separable;
-  info->spatial_rank = p->ns;
+  info->spatial_rank = p->ns ? p->ns : p->rank;
+  info->spatial_passes = p->ns ? 1 : p->n_pass;
   info->nbx = p->nbx;
   info->nby = p->nby;
   for (int i = 0; i < p->nbx; ++i) {
@@ -510,6 +673,31 @@ extern "C" bf_status bf_plan_get_info(const bf_plan* p, bf_plan_info* info) {
   info->radius = p->radius;
   info->intensity_max = p->D;
   info->input_dtype = p->input_dtype;
+  return BF_OK;
+}
+
+extern "C" bf_status bf_plan_spatial_kernel(const bf_plan* p, double* K, size_t n_values) {
+  if (!p || !K) return BF_ERR_INVALID_ARG;
+  const int r = p->radius, n = 2 * r + 1;
+  if (n_values < (size_t)n * n) return BF_ERR_INVALID_ARG;
+  if (p->ns == 0 && p->n_pass == 0) return BF_ERR_UNSUPPORTED;
+  std::fill(K, K + (size_t)n * n, 0.0);
+  const int nt = p->ns > 0 ? p->ns : p->n_pass;
+  for (int t = 0; t < nt; ++t) {
+    const bool gen = p->ns == 0;
+    const int nbx = gen ? p->pass[t].nbx : p->snbx[t], nby = gen ? p->pass[t].nby : p->snby[t];
+    std::vector<double> fx(n, 0.0), fy(n, 0.0);
+    for (int b = 0; b < nbx; ++b) {
+      const int lo = gen ? p->pass[t].lox[b] : p->slox[t][b], hi = gen ? p->pass[t].hix[b] : p->shix[t][b];
+      for (int u = lo; u <= hi; ++u) fx[u + r] += gen ? p->pass[t].wx[b] : p->swx[t][b];
+    }
+    for (int b = 0; b < nby; ++b) {
+      const int lo = gen ? p->pass[t].loy[b] : p->sloy[t][b], hi = gen ? p->pass[t].hiy[b] : p->shiy[t][b];
+      for (int v = lo; v <= hi; ++v) fy[v + r] += gen ? p->pass[t].wy[b] : p->swy[t][b];
+    }
+    for (int v = 0; v < n; ++v)
+      for (int u = 0; u < n; ++u) K[(size_t)v * n + u] += fy[v] * fx[u];
+  }
   return BF_OK;
 }
 

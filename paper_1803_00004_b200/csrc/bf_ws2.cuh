@@ -15,12 +15,15 @@
 // 0 at a 384-column halo) with 8 terms per CTA.
 //
 // CL: the range terms are split over a cluster of G CTAs on the same strip and band (CTA c owns
-// terms [c tpc, c tpc + tpc)): every CTA computes its partial int64 num / den per output pixel;
-// CTAs 1..G-1 send them to CTA 0 with st.async into CTA 0's shared memory (distributed shared
-// memory), completing CTA 0's per-row-parity mbarrier FULL[b] by transaction bytes; CTA 0 adds
-// them (exact integers: the result is bitwise that of one CTA doing all terms) and releases the
-// slot through the senders' EMPTY[b] mbarriers. No HBM workspace and one launch for up to
-// G * tpc terms (cfg4: 24 terms = 3 CTAs x 8).
+// terms [c tpc, c tpc + tpc)): every CTA computes its partial int64 (num_b, den_b) per output
+// pixel; CTAs 1..G-1 add them into CTA 0's per-row-parity slot with red.async.add (distributed
+// shared memory, exact integer adds in any order), completing CTA 0's mbarrier FULL[b] by
+// transaction bytes; CTA 0 adds the slot to its own partials (the result is bitwise that of one
+// CTA doing all terms), clears it and releases it through the senders' EMPTY[b] mbarriers. No HBM
+// workspace and one launch for up to G * tpc terms (cfg4: 24 terms = 3 CTAs x 8).
+//
+// PB (one range plan): num / den are accumulated per horizontal box b, num_b = sum W H_b with the
+// exact box sums H_b, and combined as sum_b ax_b num_b in fp64 at the end (no rounded F).
 //
 // DUMP (bf_precompute, Case 1 of P:1200-1219): FH writes the box-filtered channels F of its pixel
 // to the cache planes instead of combining them.
@@ -67,6 +70,12 @@ __device__ __forceinline__ void st_async_pair(unsigned raddr, long long a, long 
                "l"(a), "l"(b), "r"(rmbar)
                : "memory");
 }
+// exact int64 add into another CTA's shared memory, completing its mbarrier by 8 transaction bytes
+__device__ __forceinline__ void red_async_add(unsigned raddr, long long v, unsigned rmbar) {
+  asm volatile("red.async.relaxed.cluster.shared::cluster.mbarrier::complete_tx::bytes.add.u64 [%0], %1, [%2];" ::"r"(raddr),
+               "l"(v), "r"(rmbar)
+               : "memory");
+}
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -84,13 +93,14 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   constexpr int H0 = 0, S0 = NFH, V0 = NFH + NSW;
   static_assert(V0 + W2_V == W2_THREADS, "role sizes");
   constexpr int UP = w2_up(COLS);
+  constexpr bool PB = NPL == 1 && !DUMP;   // per-box accumulators (see the FH role)
   constexpr int VREG = NPL > 1 ? 104 : 112, OREG = NPL > 1 ? 56 : 48;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem_raw);   // FULL[2], EMPTY[2]
   int* Ubuf = reinterpret_cast<int*>(smem_raw + MBAR_BYTES);                     // [2][4 nk][UP]
   float2* lut = reinterpret_cast<float2*>(smem_raw + P.l_off);
   double2* lut64 = reinterpret_cast<double2*>(lut + 256);
-  longlong2* red = reinterpret_cast<longlong2*>(smem_raw + P.r_off);              // [2][G-1][TW]
+  longlong2* red = reinterpret_cast<longlong2*>(smem_raw + P.r_off);              // [2][TW][2]: sum of the senders' (num_b, den_b)
 
   const int tid = threadIdx.x;
   const int G = CL ? P.G : 1;
@@ -118,6 +128,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       mbar_init(smem_u32(&mbar[3]), NFH / 32);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    for (int i = tid; i < 2 * 2 * P.TW; i += W2_THREADS) red[i] = make_longlong2(0, 0);   // both slots
     cluster_sync();
   } else {
     __syncthreads();
@@ -226,8 +237,9 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       const int b = (y - y0) & 1;
       const float Ic = Inext;
       if (act && y + 1 < yend) Inext = load_pixel(in, U8, prow + (long long)(y + 1) * P.W);
-      long long num[NPL] = {}, den[NPL] = {};
-      int mass = 0;   // F of the k = 0 cosine channel (the clipped spatial mass) for the repair flag
+      // PB: per-box exact accumulators num_b = sum W H_b, den_b (no F rounding); num = sum_b ax_b num_b
+      long long num[PB ? 2 : NPL] = {}, den[PB ? 2 : NPL] = {};
+      double mass = 0.0;   // sum_b ax_b H_b of the k = 0 cosine channel (the clipped spatial mass)
       if (wact) {
         double c1, s1;
         pixel_angle<U8>(P, lut64, Ic, c1, s1);
@@ -244,22 +256,45 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
               if (!CONSEC)
                 for (int j = 1; j < P.kstep[t0 + i]; ++j) gk.step();
             }
-            int F[4];
+            int h0[4], h1[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const int* q = Qb + (4 * i + c) * UP;
-              long long f = mad_wide(q[e0] - q[l0], ax0, FRND);
-              if (M == 2) f = mad_wide(q[e1] - q[l1], ax1, f);
-              F[c] = fhi(f);
+              h0[c] = q[e0] - q[l0];
+              h1[c] = (M == 2) ? q[e1] - q[l1] : 0;
             }
-            if (P.kval[t0 + i] == 0) mass = F[0];
+            if (i == 0 && k0 == 0) mass = fma((double)h1[0], (double)ax1, (double)h0[0] * (double)ax0);
             if constexpr (DUMP) {
               if (act) {
                 int* cp = P.cache + (long long)(4 * P.kval[t0 + i]) * P.cache_plane + (long long)y * P.W + x0 + o;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) cp[c * P.cache_plane] = F[c];
+                for (int c = 0; c < 4; ++c) {
+                  long long f = mad_wide(h0[c], ax0, FRND);
+                  if (M == 2) f = mad_wide(h1[c], ax1, f);
+                  cp[c * P.cache_plane] = fhi(f);
+                }
+              }
+            } else if constexpr (PB) {
+              const int wc = __double2loint(fma(gk.c, P.aw[0][t0 + i], MAGIC64));
+              const int wsn = __double2loint(fma(gk.s, P.aw[0][t0 + i], MAGIC64));
+              den[0] = mad_wide(wc, h0[0], den[0]);
+              den[0] = mad_wide(wsn, h0[1], den[0]);
+              num[0] = mad_wide(wc, h0[2], num[0]);
+              num[0] = mad_wide(wsn, h0[3], num[0]);
+              if (M == 2) {
+                den[1] = mad_wide(wc, h1[0], den[1]);
+                den[1] = mad_wide(wsn, h1[1], den[1]);
+                num[1] = mad_wide(wc, h1[2], num[1]);
+                num[1] = mad_wide(wsn, h1[3], num[1]);
               }
             } else {
+              int F[4];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                long long f = mad_wide(h0[c], ax0, FRND);
+                if (M == 2) f = mad_wide(h1[c], ax1, f);
+                F[c] = fhi(f);
+              }
 #pragma unroll
               for (int q = 0; q < NPL; ++q) {   // Case 1 (bf_apply_multi): every plan over the same F
                 const int wc = __double2loint(fma(gk.c, P.aw[q][t0 + i], MAGIC64));
@@ -288,33 +323,43 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
           if (wact) {
             if (y - y0 >= 2) mbar_wait(smem_u32(&mbar[2 + b]), ph ^ 1);
             if (act) {
-              const unsigned dst = map_rank(red_l + (unsigned)(((b * (G - 1) + rank - 1) * P.TW + o) * 16), 0);
-              st_async_pair(dst, num[0], den[0], map_rank(full_l + 8 * b, 0));
+              const unsigned dst = map_rank(red_l + (unsigned)((b * P.TW + o) * 32), 0);
+              const unsigned fb = map_rank(full_l + 8 * b, 0);
+              red_async_add(dst, num[0], fb);
+              red_async_add(dst + 8, den[0], fb);
+              red_async_add(dst + 16, num[1], fb);
+              red_async_add(dst + 24, den[1], fb);
             }
           }
         } else {
-          if (o == 0) mbar_expect(full_l + 8 * b, (unsigned)((G - 1) * TWv * 16));
+          if (o == 0) mbar_expect(full_l + 8 * b, (unsigned)((G - 1) * TWv * 32));
           if (wact) {
             mbar_wait(full_l + 8 * b, ph);
             if (act) {
-#pragma unroll 1
-              for (int s = 0; s < G - 1; ++s) {
-                const longlong2 v = red[(b * (G - 1) + s) * P.TW + o];
-                num[0] += v.x;
-                den[0] += v.y;
-              }
-              finish_pixel(P, num[0], den[0], Ic, prow + (long long)y * P.W, out, ws, true, mass);
+              // the senders' partials, added exactly in CTA 0's slot (integer adds: any order)
+              longlong2* r2 = red + 2 * (b * P.TW + o);
+              const longlong2 v0 = r2[0], v1 = r2[1];
+              r2[0] = make_longlong2(0, 0);   // cleared for row y + 2 (ordered before the release below)
+              r2[1] = make_longlong2(0, 0);
+              num[0] += v0.x;
+              den[0] += v0.y;
+              num[1] += v1.x;
+              den[1] += v1.y;
+              finish_pixel_pb(P, num, den, ax0, ax1, Ic, prow + (long long)y * P.W, out, mass, ws);
             }
           }
           __syncwarp();
           if ((tid & 31) == 0)
             for (int s = 1; s < G; ++s) mbar_arrive_remote(map_rank(smem_u32(&mbar[2 + b]), s));
         }
+      } else if constexpr (PB) {
+        if (act) finish_pixel_pb(P, num, den, ax0, ax1, Ic, prow + (long long)y * P.W, out, mass, ws);
       } else {
         if (act) {
 #pragma unroll
           for (int q = 0; q < NPL; ++q)
-            finish_pixel(P, num[q], den[q], Ic, prow + (long long)y * P.W + q * P.plan_stride, out, ws, q == 0, mass);
+            finish_pixel(P, num[q], den[q], Ic, prow + (long long)y * P.W + q * P.plan_stride, out, ws, q == 0,
+                         (int)ldexp(mass, -32));
         }
       }
     }

@@ -33,7 +33,7 @@ def test_header_declares_expected_api():
                                          "bf_workspace_size", "bf_apply_batched", "bf_apply_host",
                                          "bf_apply_config", "bf_apply_launches", "bf_apply_multi",
                                          "bf_cache_size", "bf_precompute", "bf_apply_cached",
-                                         "bf_status_string", "bf_version"])
+                                         "bf_plan_spatial_kernel", "bf_status_string", "bf_version"])
 
 
 def test_library_exports_every_declared_symbol(bfmod):
@@ -254,3 +254,24 @@ def test_literal_plan_matches_oracle(bfmod, cfg, over):
     assert info["k"] == op.rng.k
     amax = max(abs(x) for x in op.rng.a)
     assert np.max(np.abs(np.array(info["a"]) - np.array(op.rng.a))) <= 1e-12 * amax
+
+
+@pytest.mark.parametrize("n_spatial,levels,radius", [(13, 4, 9), (16, 4, 24), (17, 4, 48), (25, 4, 9), (25, 2, 24),
+                                                     (36, 4, 48), (49, 4, 9), (64, 2, 9), (5, 4, 192), (9, 4, 48)])
+def test_spatial_kernel_factorisation_matches_oracle_lowering(bfmod, n_spatial, levels, radius):
+    """NEXT f3: every spatial plan the GPU path runs is a sum of separable
+    box products (one for N_s = 9, the rank-2 box-pair form for N_s = 5, otherwise the exact rank-R
+    passes of bf_plan.cpp: general_passes). Their sum must equal the oracle's independent Appendix-A
+    lowering (oracle.fit.spatial_kernel_values of the boxes of eq:2D_box_N_terms) on every offset."""
+    sigma = radius / 3.0
+    plan = bfmod.Plan(spatial="gaussian", range_kind="gaussian", sigma_s=sigma, sigma_r=20.0, radius=radius,
+                      n_terms=4, n_spatial=n_spatial, haar_levels=levels)
+    info = plan.info()
+    K = plan.spatial_kernel()
+    ref = fit.spatial_kernel_values(fit.fit_spatial("gaussian", sigma, radius, n_spatial, levels))
+    assert np.max(np.abs(K - ref)) <= 1e-12 * np.max(np.abs(ref))
+    assert info["spatial_passes"] >= 1 and info["spatial_rank"] >= 1
+    if n_spatial == 9 or (n_spatial in (25, 64) and levels == 2):
+        assert info["spatial_rank"] == 1                 # separable (Form 2 / Form 4)
+    if n_spatial not in (5, 9) and levels == 4:
+        assert info["spatial_rank"] == np.linalg.matrix_rank(ref, tol=1e-10 * np.max(np.abs(ref)))

@@ -107,10 +107,11 @@ def test_fallback_counter_and_mask_cfg3_frame12(gpu):
                         dict(range_kind="tukey", sigma_r=0.16, n_terms=12)]),
     ("cfg0", 256, 256, [dict(sigma_r=15.0), dict(sigma_r=30.0, n_terms=16), dict(range_kind="tukey", sigma_r=40.0)]),
 ])
-def test_case1_cache_bitwise_and_parity(gpu, cfg, H, W, variants):
+def test_case1_cache_matches_apply_and_oracle(gpu, cfg, H, W, variants):
     """Case 1: the box-filtered channels of k < k_count computed once
     (bf_precompute); each range plan chosen afterwards is a combine-only pass (bf_apply_cached)
-    whose output equals bf_apply's bitwise and the oracle's within the tolerance."""
+    whose output matches the oracle within the tolerance, and bf_apply to the rounding of the
+    cached F = round(sum_b ax_b H_b / 2^32) (bf_apply keeps the per-box sums exact)."""
     pkg, torch = gpu
     spec = CONFIGS[cfg]
     img = config_input(spec, H=H, W=W)
@@ -122,7 +123,8 @@ def test_case1_cache_bitwise_and_parity(gpu, cfg, H, W, variants):
         assert max(gp.info()["k"]) < 32
         got = cache.apply(gp).cpu().numpy()
         want = pkg.bilateral_filter(gp, t).cpu().numpy()
-        assert np.array_equal(got, want), v
+        e = np.abs(got.astype(np.float64) - want) * (255.0 / spec.intensity_max)
+        assert float(e.max()) <= 1e-4 and float(np.sqrt(np.mean(e * e))) <= 1e-5, (v, float(e.max()))
         parity(got, bf.bf_box(img, op), spec.intensity_max, f"{cfg} {v}")
     other, _ = plans(pkg, spec, sigma_s=2.0, radius=6)
     with pytest.raises(pkg.BFError):
@@ -140,7 +142,9 @@ def test_case2_lut_equals_direct_trig(gpu, cfg, H, W):
     lut = gpu_out(pkg, torch, gp, img, kernel="band")
     direct = gpu_out(pkg, torch, gp, img, kernel="band", u8_trig="direct")
     assert np.array_equal(lut, direct)
-    assert np.array_equal(lut, gpu_out(pkg, torch, gp, img))
+    # the default kernel (2b: per-box sums, no rounded F) agrees to F's rounding
+    e = np.abs(lut.astype(np.float64) - gpu_out(pkg, torch, gp, img))
+    assert float(e.max()) <= 1e-4 and float(np.sqrt(np.mean(e * e))) <= 1e-5
 
 
 @pytest.mark.parametrize("cfg,H,W,over,want", [
@@ -176,12 +180,13 @@ def test_two_columns_forced_on_cfg2(gpu):
     parity(gpu_out(pkg, torch, gp, img, kernel="ws2wide"), bf.bf_box(img, op), 1.0, "cfg2 ws2wide")
 
 
-@pytest.mark.parametrize("cfg,H,W,over", [("cfg2", 180, 250, {}), ("cfg0", 200, 240, {}),
-                                          ("cfg1", 170, 260, {"n_spatial": 5}), ("cfg4", 230, 210, {})])
+@pytest.mark.parametrize("cfg,H,W,over", [("cfg2", 150, 210, {}), ("cfg0", 160, 200, {}),
+                                          ("cfg1", 150, 210, {"n_spatial": 5}), ("cfg4", 170, 190, {})])
 def test_repair_pass_alone_reproduces_oracle(gpu, cfg, H, W, over):
     """With the repair threshold above every pixel's conditioning, every pixel is re-evaluated by
     the fp64 repair pass (the direct double loop of pin P1): the output then equals the oracle's
-    to float32 rounding, including its fallback pixels."""
+    to float32 rounding, including its fallback pixels. (Images of <= 32768 pixels: the repair
+    list's capacity per call.)"""
     pkg, torch = gpu
     spec = CONFIGS[cfg]
     img = config_input(spec, H=H, W=W)
