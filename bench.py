@@ -154,7 +154,9 @@ def config_dict(spec, flush: bool, world: int, n_spatial: int) -> dict:
                         f"K_r {spec.range_kind} sigma_r={spec.sigma_r}, N={spec.n_terms}, D={spec.intensity_max}",
             "H": spec.H, "W": spec.W, "frames_per_step": frames_per_step(spec), "n_spatial": n_spatial,
             "l2": "flushed (256 MiB write) before every timed step" if flush else "not flushed",
-            "parallelism": f"dp{world} (independent images per rank)" if world > 1 else "single GPU"}
+            "parallelism": ("single GPU" if world == 1 else
+                            f"{world} ranks, the {spec.frames} frames sharded (bf_shard_frames)" if spec.frames > 1
+                            else f"dp{world} (independent images per rank)")}
 
 
 # --------------------------------------------------------------------------------------------
@@ -229,17 +231,29 @@ def committed_json(name: str):
     return json.load(open(p)) if os.path.exists(p) else None
 
 
+def rank_frames(pkg, spec, world: int, rank: int) -> range:
+    """Frames this rank filters: single-image configs replicate the image on every rank (weak
+    scaling); a frame stream (cfg3) is sharded, every frame on exactly one rank (bf_shard_frames,
+    strong scaling, no data-path collective)."""
+    if spec.frames == 1 or world == 1:
+        return range(spec.frames)
+    first, count = pkg.shard_frames(spec.frames, world, rank)
+    return range(first, first + count)
+
+
 class Workload:
     """One BASELINE config resident on the device: inputs, outputs, plan, the step callable."""
 
-    def __init__(self, pkg, torch, spec, dev, n_spatial: int):
+    def __init__(self, pkg, torch, spec, dev, n_spatial: int, frames: range = None):
         from synth import config_input
         self.spec = spec
         self.plan = pkg.Plan(spatial=spec.spatial, range_kind=spec.range_kind, sigma_s=spec.sigma_s,
                              sigma_r=spec.sigma_r, radius=spec.radius, n_terms=spec.n_terms,
                              intensity_max=spec.intensity_max, n_spatial=n_spatial,
                              input_dtype="u8" if is_u8(spec) else "f32")
-        self.frames = [config_input(spec, frame=f) for f in range(spec.frames)]
+        self.frame_ids = frames if frames is not None else range(spec.frames)
+        self.nf = len(self.frame_ids)
+        self.frames = [config_input(spec, frame=f) for f in self.frame_ids]
         self.inp = torch.from_numpy(self.frames[0] if spec.frames == 1 else __import__("numpy").stack(self.frames)).to(dev)
         self.out = torch.empty(self.inp.shape, dtype=torch.float32, device=dev)
         self.H, self.W = spec.H, spec.W
@@ -257,15 +271,16 @@ class Workload:
                                   repaired_count=self.rep.data_ptr() if counters else 0)
 
     def step(self, stream, args=None):
-        """One step: every frame through bf_apply_ex (cfg3: 64 calls on one stream)."""
+        """One step: every frame of this rank through bf_apply_ex (cfg3: one call per frame on one
+        stream)."""
         n = self.H * self.W
         esz = self.inp.element_size()
-        for f in range(self.spec.frames):
+        for f in range(self.nf):
             self.pkg.apply_ex(self.plan, self.inp.data_ptr() + f * n * esz, self.out.data_ptr() + f * n * 4, 1,
                               self.H, self.W, stream, args)
 
     def step_batched(self, stream, args=None):
-        self.pkg.apply_ex(self.plan, self.inp.data_ptr(), self.out.data_ptr(), self.spec.frames, self.H, self.W,
+        self.pkg.apply_ex(self.plan, self.inp.data_ptr(), self.out.data_ptr(), self.nf, self.H, self.W,
                           stream, args)
 
 
@@ -302,8 +317,9 @@ def alu_channels(plan) -> int:
     return 4 * len(ks) - (2 if 0 in ks else 0)
 
 
-def bench_one(pkg, torch, spec, dev, stream, flush, args, steps, warmup, peaks, sampler=None, n_spatial=9):
-    wl = Workload(pkg, torch, spec, dev, n_spatial)
+def bench_one(pkg, torch, spec, dev, stream, flush, args, steps, warmup, peaks, sampler=None, n_spatial=9,
+              frames=None):
+    wl = Workload(pkg, torch, spec, dev, n_spatial, frames)
     sptr = stream.cuda_stream
     a = wl.args()
     times = timed(torch, stream, lambda: wl.step(sptr, a), steps, warmup, flush, sampler)
@@ -313,12 +329,12 @@ def bench_one(pkg, torch, spec, dev, stream, flush, args, steps, warmup, peaks, 
     kt = timed(torch, stream, lambda: wl.step(sptr, a0), max(3, steps // 2), 2, flush)
     kms = statistics.median(kt)
     cfg = pkg.config(wl.plan, spec.H, spec.W)
-    px = spec.H * spec.W * spec.frames
+    px = spec.H * spec.W * wl.nf
     bpp = (1 if is_u8(spec) else 4) + 4
     C = alu_channels(wl.plan)
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 128 * sm_mhz * 1e6
-    res = {"ms_per_step": ms, "value": px / 1e6 / (ms / 1e3), "unit": UNIT, "frames_per_step": spec.frames,
+    res = {"ms_per_step": ms, "value": px / 1e6 / (ms / 1e3), "unit": UNIT, "frames_per_step": wl.nf,
            "kernel_ms": kms, "kernel": cfg["kernel"], "launches_per_frame": cfg["launches"] + 1,
            "launch": {"threads_per_cta": cfg["threads_per_cta"], "grid": list(cfg["grid"]), "tile": list(cfg["tile"]),
                       "smem_bytes": cfg["smem_bytes"], "cluster": cfg["cluster"],
@@ -329,7 +345,21 @@ def bench_one(pkg, torch, spec, dev, stream, flush, args, steps, warmup, peaks, 
         bt = timed(torch, stream, lambda: wl.step_batched(sptr, a), steps, warmup, flush)
         res["batched_ms_per_step"] = statistics.median(bt)
         res["batched_value"] = px / 1e6 / (res["batched_ms_per_step"] / 1e3)
-        res["per_frame_ms"] = ms / spec.frames
+        res["per_frame_ms"] = ms / wl.nf
+        # the same one-call-per-frame stream captured once into a CUDA graph and replayed
+        # (NEXT f4: no per-call host overhead; bf_apply is capturable: no allocation, no sync)
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            wl.step(side.cuda_stream, a)
+        stream.wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            wl.step(side.cuda_stream, a)
+        gt = timed(torch, stream, g.replay, steps, warmup, flush)
+        res["graph_ms_per_step"] = statistics.median(gt)
+        res["graph_value"] = px / 1e6 / (res["graph_ms_per_step"] / 1e3)
+        del g
     return wl, res, times
 
 
@@ -349,13 +379,16 @@ def run_ours(args, spec):
 
     barrier(world)
     sampler = ClockSampler(local)
+    frames = rank_frames(pkg, spec, world, rank)
+    sharded = spec.frames > 1 and world > 1
     wl, head, times = bench_one(pkg, torch, spec, dev, stream, flush, args, args.steps, args.warmup, peaks, sampler,
-                                args.n_spatial)
+                                args.n_spatial, frames)
     barrier(world)
     total_ms = reduce_max(sum(times), world, dev)
     ms = total_ms / args.steps
-    px_step = spec.H * spec.W * spec.frames
-    value = world * px_step * args.steps / 1e6 / (total_ms / 1e3)
+    px_step = spec.H * spec.W * wl.nf                               # this rank's pixels per step
+    job_px = spec.H * spec.W * (spec.frames if sharded else world * spec.frames)   # all ranks together
+    value = job_px * args.steps / 1e6 / (total_ms / 1e3)
     launches = wl.pkg.launches(wl.plan, spec.H, spec.W) + 1      # fused launch(es) + the repair pass
 
     # parity: device counters of one step, the live sampled check, the committed every-pixel run
@@ -371,7 +404,7 @@ def run_ours(args, spec):
     sptr = stream.cuda_stream
 
     def e2e_step():
-        for f in range(spec.frames):
+        for f in range(wl.nf):
             pkg.apply_host(wl.plan, h_in[f].data_ptr(), h_out.data_ptr(), spec.H, spec.W, sptr)
 
     for _ in range(max(1, args.warmup // 2)):
@@ -383,7 +416,7 @@ def run_ours(args, spec):
         e2e_step()
         e2e_t.append(time.perf_counter() - t0)
     e2e_total = reduce_max(sum(e2e_t), world, dev)
-    e2e_value = world * px_step * args.steps / 1e6 / e2e_total
+    e2e_value = job_px * args.steps / 1e6 / e2e_total
 
     if rank != 0:
         barrier(world)
@@ -405,7 +438,8 @@ def run_ours(args, spec):
     kms = head["kernel_ms"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f32 channels, i32 box sums, i64 combine (fp64 repair)", "data": "synthetic",
         "config": config_dict(spec, True, world, args.n_spatial),
         "roofline": {"bound": "alu", "achieved": alu_ops / (kms / 1e3) / 1e12, "peak": alu_peak,
@@ -421,9 +455,9 @@ def run_ours(args, spec):
                          "frac": alg_bytes / (kms / 1e3) / 1e9 / hbm_peak, "algorithmic_bytes_per_step": alg_bytes,
                          "peak_source": peaks["_source"] + " hbm_gbs",
                          "note": "BASELINE metric: image bytes in + out at the measured HBM bandwidth"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(wl.frames[0].nbytes) * spec.frames,
-                "d2h_bytes_per_step": int(spec.H * spec.W * 4) * spec.frames},
-        "gpu_launches": args.steps * launches * spec.frames,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(wl.frames[0].nbytes) * wl.nf,
+                "d2h_bytes_per_step": int(spec.H * spec.W * 4) * wl.nf},
+        "gpu_launches": args.steps * launches * wl.nf,
         "clocks": clocks,
         "parity": parity,
     }

@@ -199,11 +199,12 @@ typedef struct {
 } bf_apply_args;
 
 /* Default bf_apply_args.repair_threshold: out = num / den magnifies the fused kernels' rounding
- * (channel values in fp32, 22-bit tap quantisation) by 1 / cond: measured |error| ~ 4e-6 / cond on
- * the [0, 255] scale over the BASELINE configs at full size, i.e. the 1e-3 parity tolerance is
- * reached near cond = 0.004; the default re-evaluates every pixel below twice that. At most 32768
- * flagged pixels per call are repaired (the rest keep the fused value); up to 16 calls may be in
- * flight per device. */
+ * (channel values in fp32, 22-bit tap quantisation) by 1 / cond. Measured over the BASELINE configs
+ * at full size, |error| * cond <= 2.3e-7 * kmax on the [0, 255] scale (kmax = the largest selected
+ * frequency: the fp32 channels' phase error grows with k), so the 1e-3 parity tolerance is reached
+ * near cond = 2.3e-4 kmax; the default (threshold 0) re-evaluates every pixel below
+ * max(BF_REPAIR_DEFAULT, 4.6e-4 kmax), twice that. At most 32768 flagged pixels per call are
+ * repaired (the rest keep the fused value); up to 16 calls may be in flight per device. */
 #define BF_REPAIR_DEFAULT 0.008
 
 BF_API void bf_apply_args_default(bf_apply_args* args);
@@ -228,6 +229,15 @@ BF_API bf_status bf_workspace_size(const bf_plan* plan, int n_frames, int H, int
  */
 BF_API bf_status bf_apply_batched(const bf_plan* plan, const void* d_in, float* d_out, int n_frames, int H, int W,
                            bf_stream stream);
+
+/*
+ * Frame sharding for multi-GPU frame streams (NEXT f4; BASELINE configs[3]): frames are independent
+ * problems, so N GPUs (one process per GPU) each filter a contiguous block of them with
+ * bf_apply_batched / bf_apply_ex on their own device, with no data-path collective. Part `part`
+ * of n_parts gets frames [*first, *first + *count): contiguous blocks, the first
+ * n_frames % n_parts parts one frame longer, every frame exactly once. Pure host computation.
+ */
+BF_API bf_status bf_shard_frames(int n_frames, int n_parts, int part, int* first, int* count);
 
 /*
  * Case 1 of the paper's pre-computation: with T_{r_i} = D for every range kernel,

@@ -11,11 +11,11 @@ streams; every step of the filter runs in the library's host fitter and sm_100a 
 from __future__ import annotations
 
 from ._bf import (BFError, CacheDesc, Plan, apply, apply_batched, apply_cached, apply_ex, apply_host, apply_multi,
-                  cache_size, config, launches, lib, make_args, precompute, version, workspace_size)
+                  cache_size, config, launches, lib, make_args, precompute, shard_frames, version, workspace_size)
 
 __all__ = ["BFError", "CacheDesc", "Plan", "apply", "apply_batched", "apply_cached", "apply_ex", "apply_host",
            "apply_multi", "bilateral_filter", "bilateral_filter_multi", "cache_size", "config", "launches", "lib",
-           "make_args", "precompute", "version", "workspace_size", "RangeCache"]
+           "make_args", "precompute", "shard_frames", "version", "workspace_size", "RangeCache"]
 
 
 def _check_tensor(t, plan):

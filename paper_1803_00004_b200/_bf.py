@@ -25,7 +25,7 @@ RANGE = {"gaussian": BF_RANGE_GAUSSIAN, "tukey": BF_RANGE_TUKEY}
 #: every symbol include/bf.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bf_plan_options_default", "bf_plan_create", "bf_plan_destroy", "bf_plan_get_info", "bf_apply",
            "bf_apply_args_default", "bf_apply_ex", "bf_workspace_size", "bf_apply_batched", "bf_apply_config",
-           "bf_apply_host", "bf_apply_launches", "bf_apply_multi", "bf_cache_size", "bf_precompute", "bf_plan_spatial_kernel",
+           "bf_apply_host", "bf_apply_launches", "bf_apply_multi", "bf_cache_size", "bf_precompute", "bf_plan_spatial_kernel", "bf_shard_frames",
            "bf_apply_cached", "bf_status_string", "bf_version")
 BF_MAX_PLANS = 4
 
@@ -122,6 +122,8 @@ def lib() -> C.CDLL:
         L.bf_precompute.restype = C.c_int
         L.bf_apply_cached.argtypes = [P, C.POINTER(CacheDesc), P, P, P, P, C.POINTER(ApplyArgs)]
         L.bf_apply_cached.restype = C.c_int
+        L.bf_shard_frames.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.bf_shard_frames.restype = C.c_int
         L.bf_plan_spatial_kernel.argtypes = [P, C.POINTER(C.c_double), C.c_size_t]
         L.bf_plan_spatial_kernel.restype = C.c_int
         L.bf_status_string.argtypes = [C.c_int]
@@ -302,6 +304,13 @@ def config(plan: Plan, H: int, W: int, n_frames: int = 1, args: ApplyArgs | None
             "grid": (c.grid_x, c.grid_y, c.grid_z), "tile": (c.tile_w, c.tile_h), "smem_bytes": c.smem_bytes,
             "cluster": c.cluster_size, "terms_per_cta": c.terms_per_cta, "cols_per_thread": c.cols_per_thread,
             "workspace_bytes": c.workspace_bytes}
+
+
+def shard_frames(n_frames: int, n_parts: int, part: int) -> tuple:
+    """(first, count): the contiguous block of frames part `part` of n_parts filters (bf_shard_frames)."""
+    f, c = C.c_int(), C.c_int()
+    _check(lib().bf_shard_frames(int(n_frames), int(n_parts), int(part), C.byref(f), C.byref(c)), "bf_shard_frames")
+    return f.value, c.value
 
 
 def version() -> str:

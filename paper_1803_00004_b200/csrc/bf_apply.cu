@@ -280,6 +280,33 @@ void repair_params(const bf_plan* const* plans, int nplans, int n_frames, int H,
     amax = std::max(amax, as);
   }
   R.qscale = std::ldexp(1.0, 61) / std::max(1e-300, sabs * amax * std::max(1.0, p->D));
+  // piecewise Taylor table of K~_r (f32 input, one plan): K~_r(t) = sum_k a_k cos(w k t), w = pi / T;
+  // on [c - h, c + h] with w kmax h <= 1/2 the degree-13 remainder is < 0.5^14 / 14! sum |a_k|
+  R.ntab = 0;
+  if (!R.u8 && nplans == 1) {
+    const double w = M_PI / p->T;
+    const double h = 0.5 / (w * std::max(1, R.kmax));
+    const int n = (int)std::ceil(p->D / (2.0 * h));
+    if (n >= 1 && n * (REP_DEG + 1) <= REP_TAB) {
+      R.ntab = n;
+      R.tab_h = h;
+      double fact[REP_DEG + 1];
+      fact[0] = 1.0;
+      for (int m = 1; m <= REP_DEG; ++m) fact[m] = fact[m - 1] * m;
+      for (int i = 0; i < n; ++i) {
+        const double c = (2 * i + 1) * h;
+        for (int m = 0; m <= REP_DEG; ++m) {
+          double v = 0.0;
+          for (int j = 0; j < p->n_k; ++j) {
+            const double kw = w * p->k[j];
+            // d^m/dt^m cos(kw t) = kw^m cos(kw t + m pi / 2)
+            v += p->a[j] * std::pow(kw, m) / fact[m] * std::cos(kw * c + m * M_PI_2);
+          }
+          R.tab[i * (REP_DEG + 1) + m] = v;
+        }
+      }
+    }
+  }
   R.count = S.count;
   R.list = S.list;
   R.acc = S.acc;
@@ -290,10 +317,22 @@ void repair_params(const bf_plan* const* plans, int nplans, int n_frames, int H,
 }
 
 // Claims a repair slot for one call and clears its counter on the stream (graph capturable).
-bf_status repair_sink(const bf_apply_args& A, double wscale, double mfull, cudaStream_t st, RepairSink& S) {
+// The default repair threshold of a set of range plans: the fused kernels' error grows about
+// linearly with the largest frequency (the fp32 channels' phase error), measured |err| * cond
+// <= 2.3e-7 kmax on the [0, 255] scale over the full-size BASELINE configs; twice that margin
+// against the 1e-3 tolerance, never below BF_REPAIR_DEFAULT.
+double default_tau(const bf_plan* const* plans, int nplans) {
+  int kmax = 0;
+  for (int q = 0; q < nplans; ++q)
+    for (int i = 0; i < plans[q]->n_k; ++i) kmax = std::max(kmax, plans[q]->k[i]);
+  return std::max(BF_REPAIR_DEFAULT, 4.6e-4 * kmax);
+}
+
+bf_status repair_sink(const bf_apply_args& A, double wscale, double mfull, double tau_default, cudaStream_t st,
+                      RepairSink& S) {
   std::memset(&S, 0, sizeof(S));
   if (A.repair_threshold < 0) return BF_OK;
-  const double tau = A.repair_threshold > 0 ? A.repair_threshold : BF_REPAIR_DEFAULT;
+  const double tau = A.repair_threshold > 0 ? A.repair_threshold : tau_default;
   const unsigned slot = g_repair_ticket.fetch_add(1, std::memory_order_relaxed) % REPAIR_SLOTS;
   if (repair_slot(slot, &S.count, &S.list, &S.acc) != cudaSuccess) return BF_ERR_CUDA;
   if (cudaMemsetAsync(S.count, 0, sizeof(unsigned), st) != cudaSuccess) return BF_ERR_CUDA;
@@ -768,7 +807,7 @@ bf_status run_general(const Req& R, const bf_plan* const* plans, int nplans, con
     mass_abs += fx * fy;
   }
   RepairSink S;
-  const bf_status rs = repair_sink(A, 1.0, mass_abs, st, S);
+  const bf_status rs = repair_sink(A, 1.0, mass_abs, default_tau(plans, nplans), st, S);
   if (rs != BF_OK) return rs;
   int gl = 0;
   cudaError_t err = cudaSuccess;
@@ -871,7 +910,7 @@ bf_status run(const bf_plan* const* plans, int nplans, const void* d_in, float* 
   L.P.fb_count = A.d_fallback_count;
   L.P.fb_mask = A.d_fallback_mask;
   if (!dump) {
-    const bf_status rs = repair_sink(A, std::ldexp(1.0, wbits), mass_full(p, L.P), st, L.P.rep);
+    const bf_status rs = repair_sink(A, std::ldexp(1.0, wbits), mass_full(p, L.P), default_tau(plans, nplans), st, L.P.rep);
     if (rs != BF_OK) return rs;
   }
   int gl = 0;
@@ -980,6 +1019,15 @@ extern "C" bf_status bf_workspace_size(const bf_plan* plan, int n_frames, int H,
   return s;
 }
 
+extern "C" bf_status bf_shard_frames(int n_frames, int n_parts, int part, int* first, int* count) {
+  if (!first || !count || n_frames < 0 || n_parts < 1 || part < 0 || part >= n_parts) return BF_ERR_INVALID_ARG;
+  // contiguous blocks, the first n_frames % n_parts parts one frame longer
+  const int base = n_frames / n_parts, extra = n_frames % n_parts;
+  *count = base + (part < extra ? 1 : 0);
+  *first = part * base + std::min(part, extra);
+  return BF_OK;
+}
+
 extern "C" bf_status bf_apply(const bf_plan* plan, const void* d_in, float* d_out, int H, int W, bf_stream stream) {
   return run(&plan, 1, d_in, d_out, 1, H, W, reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr);
 }
@@ -1082,7 +1130,7 @@ extern "C" bf_status bf_apply_cached(const bf_plan* plan, const bf_cache_desc* d
   KParams Q;
   std::memset(&Q, 0, sizeof(Q));
   quantise(plan, Q);
-  const bf_status rs = repair_sink(A, std::ldexp(1.0, wbits), mass_full(plan, Q), st, C.rep);
+  const bf_status rs = repair_sink(A, std::ldexp(1.0, wbits), mass_full(plan, Q), default_tau(&plan, 1), st, C.rep);
   if (rs != BF_OK) return rs;
   cudaError_t err = launch_cached(C, static_cast<const int*>(d_cache), d_in, d_out, st);
   if (err == cudaSuccess && C.rep.count) {

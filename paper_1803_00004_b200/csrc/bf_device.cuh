@@ -257,6 +257,23 @@ struct Cheb64 {
   }
 };
 
+// n - 1 further steps of a recurrence (n = k_i - k_{i-1} >= 1 for non-consecutive terms), the
+// common small gaps unrolled (a counted loop costs register moves and branches per step)
+template <class F>
+__device__ __forceinline__ void extra_steps(int n, F&& step) {
+  if (n > 1) {
+    step();
+    if (n > 2) {
+      step();
+      if (n > 3) {
+        step();
+#pragma unroll 1
+        for (int j = 4; j < n; ++j) step();
+      }
+    }
+  }
+}
+
 // Spatial forms the kernels are instantiated for: NS box-pair terms, NBY vertical boxes (shared
 // taps), NBX horizontal boxes per term.
 template <int FORM>
@@ -410,9 +427,10 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
 #pragma unroll
         for (int b = 0; b < NB; ++b) g2[b].step();
         if (!CONSEC)
-          for (int j = 1; j < P.kstep[t0 + i]; ++j)
+          extra_steps(P.kstep[t0 + i], [&] {
 #pragma unroll
             for (int b = 0; b < NB; ++b) g2[b].step();
+          });
       }
 #pragma unroll
       for (int b = 0; b < NB; ++b) {

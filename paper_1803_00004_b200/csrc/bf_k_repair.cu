@@ -11,8 +11,9 @@
 // mathematically. The window is cut into chunks of rows, one CTA per (pixel, chunk):
 // fp64 partial sums in a fixed order, rounded to a fixed-point int64 (|error| <= 2^-62 of the
 // whole window's absolute mass) and added exactly, so the result is deterministic. f32 inputs
-// evaluate cos(pi (I(x) - I(y)) / T) from fp64 polynomial base angles and K~_r by the Chebyshev
-// recurrence; u8 inputs tabulate K~_r on the 511 integer differences.
+// evaluate K~_r(I(x) - I(y)) from a piecewise degree-13 Taylor table (host-computed, remainder
+// < 1e-15 of sum |a_k|; where the table would be too large: fp64 polynomial base angles and the
+// Chebyshev recurrence); u8 inputs tabulate K~_r exactly on the 511 integer differences.
 #include <algorithm>
 #include <atomic>
 
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(RT) bf_repair_kernel(const RParams R, const vo
   const int n1 = 2 * R.rad + 1;
   double* fx = sm;                   // [ns][n1]: fx_s(u), u = -rad..rad
   double* fy = sm + R.ns * n1;       // [ns][n1]
-  double* klut = sm + 2 * R.ns * n1; // [511] K~_r(t), t = -255..255 (u8)
+  double* klut = sm + 2 * R.ns * n1; // [511] K~_r(t), t = -255..255 (u8), or the Taylor table (f32)
   __shared__ double red[2][RT / 32];
   __shared__ int last;
   const int tid = threadIdx.x;
@@ -97,6 +98,8 @@ __global__ void __launch_bounds__(RT) bf_repair_kernel(const RParams R, const vo
   const unsigned n = min(*R.count, R.cap);
   if (R.repaired && blockIdx.x == 0 && tid == 0 && n) atomicAdd(R.repaired, (unsigned long long)n);
   const double invT = 1.0 / R.T;
+  for (int i = tid; i < R.ntab * (REP_DEG + 1); i += RT) klut[i] = R.tab[i];
+  const double inv2h = R.ntab ? 0.5 / R.tab_h : 0.0;
   int lut_q = -1;
   const unsigned long long items = (unsigned long long)n * (unsigned)R.nch;
   for (unsigned long long it = blockIdx.x; it < items; it += gridDim.x) {
@@ -146,9 +149,19 @@ __global__ void __launch_bounds__(RT) bf_repair_kernel(const RParams R, const vo
           kr = klut[(int)Ix - iy + 255];
         } else {
           Iy = (double)__ldg(reinterpret_cast<const float*>(in) + rbase + col);
-          double cy, sy;
-          angle64(Iy, invT, cy, sy);
-          kr = range_cheb(R, q, fma(cx, cy, sx * sy));   // cos(pi (Ix - Iy) / T)
+          if (R.ntab) {   // Taylor polynomial of the interval holding |Ix - Iy|
+            const double t = fabs(Ix - Iy);
+            const int i = min((int)(t * inv2h), R.ntab - 1);
+            const double s = t - (2 * i + 1) * R.tab_h;
+            const double* c = klut + i * (REP_DEG + 1);
+            kr = c[REP_DEG];
+#pragma unroll
+            for (int m = REP_DEG - 1; m >= 0; --m) kr = fma(kr, s, c[m]);
+          } else {
+            double cy, sy;
+            angle64(Iy, invT, cy, sy);
+            kr = range_cheb(R, q, fma(cx, cy, sx * sy));   // cos(pi (Ix - Iy) / T)
+          }
         }
         const double w = ks * kr;
         den += w;
@@ -221,7 +234,8 @@ cudaError_t repair_slot(unsigned s, unsigned** count, unsigned long long** list,
 }
 
 cudaError_t launch_repair(const RParams& R, const void* in, float* out, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (2 * (size_t)R.ns * (2 * (size_t)R.rad + 1) + 512);
+  const size_t smem =
+      sizeof(double) * (2 * (size_t)R.ns * (2 * (size_t)R.rad + 1) + std::max(512, R.ntab * (REP_DEG + 1)));
   cudaError_t e = cudaFuncSetAttribute(bf_repair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 148;

@@ -149,6 +149,7 @@ struct CParams {
 cudaError_t launch_cached(const CParams& C, const int* cache, const void* in, float* out, cudaStream_t st);
 
 // fp64 repair of the flagged pixels (bf_k_repair.cu).
+constexpr int REP_DEG = 13, REP_TAB = 2048;
 struct RParams {
   int H, W;
   long long frame_elems, plan_stride;
@@ -165,6 +166,12 @@ struct RParams {
   double wx[BF_MAX_SP_PASSES][MAXB], wy[BF_MAX_SP_PASSES][MAXB];
   int rad;                    // window half-width (max box extent)
   int nch, rpc;               // chunks per pixel, window rows per chunk
+  // f32, one plan: K~_r(t) for t = |I(x) - I(y)| in [0, D] as piecewise Taylor polynomials of
+  // degree REP_DEG on ntab intervals of width 2 tab_h (truncation < 1e-15 of sum |a_k|), else the
+  // Chebyshev recurrence per tap (ntab = 0)
+  int ntab;
+  double tab_h;
+  double tab[REP_TAB];
   double qscale;              // fixed-point scale of the partial sums: |den partial| * qscale < 2^61
   unsigned* count;
   const unsigned long long* list;

@@ -52,7 +52,7 @@ __device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "W%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra W%=;\n}" ::"r"(a),
       "r"(parity)
       : "memory");
@@ -148,14 +148,13 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       vwork[j] = ((vt & ~31) + j * W2_V) < wv;     // warp-uniform: this block of 32 columns is scanned
     }
     int U[COLS][NS * 4 * MAXK];
-    float Ipre[COLS][NB][2];
+    // prefetched taps: COLS == 1 the next row's; COLS == 2 the next (row, column) in the order
+    // (y, 0), (y, 1), (y + 1, 0), ... (one column's worth of registers)
+    float Ipre[NB][2];
 #pragma unroll
-    for (int j = 0; j < COLS; ++j) {
-      if (vwork[j]) {
-        v_init<MAXK, NB, NS, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, U[j]);
-        load_taps<NB, U8>(P, in, fbase, col[j], colok[j], y0, Ipre[j]);
-      }
-    }
+    for (int j = 0; j < COLS; ++j)
+      if (vwork[j]) v_init<MAXK, NB, NS, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, U[j]);
+    load_taps<NB, U8>(P, in, fbase, col[0], colok[0], y0, Ipre);
     for (int y = y0; y < yend; ++y) {
       const int b = (y - y0) & 1;
       const GroupSync hook{b, n_uempty, n_ufull, y - y0 >= 2};
@@ -165,10 +164,10 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
           float Icur[NB][2];
 #pragma unroll
           for (int bb = 0; bb < NB; ++bb) {
-            Icur[bb][0] = Ipre[0][bb][0];
-            Icur[bb][1] = Ipre[0][bb][1];
+            Icur[bb][0] = Ipre[bb][0];
+            Icur[bb][1] = Ipre[bb][1];
           }
-          if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col[0], colok[0], y + 1, Ipre[0]);
+          if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col[0], colok[0], y + 1, Ipre);
           v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP, GroupSync, CL>(P, lut, colok[0], y, t0, nkc, Icur, U[0], Ub, &hook);
         } else {
           for (int g = 0; g < ngrp; ++g) {
@@ -180,17 +179,25 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         hook.begin(0);
 #pragma unroll
         for (int j = 0; j < COLS; ++j) {
-          if (vwork[j]) {
-            float Icur[NB][2];
+          // the column's coordinates are recomputed per row (cheap) rather than held across the
+          // loop: with two 32-channel states the V role has no registers to spare
+          const int e = vt + j * W2_V;
+          const int cj = x0 - P.rlo_x + e;
+          const bool okj = (cj >= 0) & (cj < P.W) & (e < wv);
+          float Icur[NB][2];
 #pragma unroll
-            for (int bb = 0; bb < NB; ++bb) {
-              Icur[bb][0] = Ipre[j][bb][0];
-              Icur[bb][1] = Ipre[j][bb][1];
-            }
-            if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col[j], colok[j], y + 1, Ipre[j]);
-            v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP, GroupSync, CL>(P, lut, colok[j], y, t0, nkc, Icur, U[j],
-                                                                    Ub + j * W2_V);
+          for (int bb = 0; bb < NB; ++bb) {
+            Icur[bb][0] = Ipre[bb][0];
+            Icur[bb][1] = Ipre[bb][1];
           }
+          {   // prefetch the taps of the next (row, column)
+            const int jn = (j + 1) % COLS, yn = j + 1 < COLS ? y : y + 1;
+            const int en = vt + jn * W2_V, cn = x0 - P.rlo_x + en;
+            if (yn < yend) load_taps<NB, U8>(P, in, fbase, cn, (cn >= 0) & (cn < P.W) & (en < wv), yn, Ipre);
+          }
+          if (((vt & ~31) + j * W2_V) < wv)
+            v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP, GroupSync, CL>(P, lut, okj, y, t0, nkc, Icur, U[j],
+                                                                    Ub + j * W2_V);
         }
         hook.end(0);
       }
@@ -253,8 +260,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
             if ((i & 7) == 0) bar_sync(BAR_Q_FULL + 2 * b + (i >> 3), n_qfull);
             if (!DUMP && i > 0) {   // k_i - k_{i-1} >= 1 steps
               gk.step();
-              if (!CONSEC)
-                for (int j = 1; j < P.kstep[t0 + i]; ++j) gk.step();
+              if (!CONSEC) extra_steps(P.kstep[t0 + i], [&] { gk.step(); });
             }
             int h0[4], h1[4];
 #pragma unroll

@@ -33,7 +33,7 @@ def test_header_declares_expected_api():
                                          "bf_workspace_size", "bf_apply_batched", "bf_apply_host",
                                          "bf_apply_config", "bf_apply_launches", "bf_apply_multi",
                                          "bf_cache_size", "bf_precompute", "bf_apply_cached",
-                                         "bf_plan_spatial_kernel", "bf_status_string", "bf_version"])
+                                         "bf_plan_spatial_kernel", "bf_shard_frames", "bf_status_string", "bf_version"])
 
 
 def test_library_exports_every_declared_symbol(bfmod):

@@ -214,3 +214,33 @@ def test_row_range(gpu):
     f, p = full.cpu().numpy(), part.cpu().numpy()
     assert np.array_equal(p[123:311], f[123:311])
     assert np.all(np.isnan(p[:123])) and np.all(np.isnan(p[311:]))
+
+
+def test_graph_captured_frame_stream(gpu):
+    """NEXT f4 (BASELINE configs[3], "one bf_apply per frame on one stream"): a stream of per-frame
+    bf_apply calls captured once into a CUDA graph (each call claims its own repair slot at capture
+    time; on one stream the calls stay ordered) and replayed gives every frame bitwise as the eager
+    calls, which equal bf_apply_batched's frames."""
+    pkg, torch = gpu
+    spec = CONFIGS["cfg3"]
+    H, W, F = 120, 200, 20                       # more frames than repair slots (16)
+    frames = torch.from_numpy(np.stack([config_input(spec, H=H, W=W, frame=f) for f in range(F)])).cuda()
+    gp, _ = plans(pkg, spec)
+    eager = torch.stack([pkg.bilateral_filter(gp, frames[f]) for f in range(F)])
+    batched = pkg.bilateral_filter(gp, frames)
+    assert torch.equal(eager, batched)
+    out = torch.empty_like(eager)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for f in range(F):
+            pkg.bilateral_filter(gp, frames[f], out=out[f], stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for f in range(F):
+            pkg.bilateral_filter(gp, frames[f], out=out[f], stream=s)
+    out.fill_(float("nan"))
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)

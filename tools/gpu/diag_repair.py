@@ -24,7 +24,7 @@ def main():
         nf = min(spec.frames, 8)
         x = torch.from_numpy(__import__("numpy").stack([config_input(spec, frame=f) for f in range(nf)])).cuda()
         y = torch.empty(x.shape, dtype=torch.float32, device="cuda")
-        for tau in (-1.0, 0.015, 0.008, 0.004, 0.002, 0.001):
+        for tau in (-1.0, 0.0, 0.015, 0.008, 0.004, 0.002):
             rep = torch.zeros(1, dtype=torch.int64, device="cuda")
             ts = []
             for i in range(4):
