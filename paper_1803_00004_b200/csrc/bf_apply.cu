@@ -214,6 +214,20 @@ double mass_full(const bf_plan* p, const KParams& P) {
   return F / 4294967296.0;
 }
 
+// An upper bound of that channel's F for any clipped window: the absolute box weights summed
+double mass_bound(const KParams& P) {
+  double F = 0.0;
+  for (int t = 0; t < P.ns; ++t) {
+    double U = std::fabs((double)P.urnd);
+    for (int b = 0; b < P.nby; ++b) U += std::fabs(std::rint((double)P.qs[t][b])) * (P.vhi[b] - P.vlo[b] + 1);
+    const double Up = std::ceil(U / std::ldexp(1.0, P.ush)) + 1.0;
+    double X = 0.0;
+    for (int b = 0; b < P.nbx[t]; ++b) X += (P.hhi[t][b] - P.hlo[t][b] + 1) * std::fabs((double)P.ax[t][b]);
+    F += Up * X;
+  }
+  return F / 4294967296.0 * (1.0 + 1e-9);
+}
+
 std::atomic<unsigned> g_repair_ticket{0};
 
 // The repair pass's parameters for the plans of one call (spatial boxes, range terms).
@@ -339,6 +353,7 @@ bf_status repair_sink(const bf_apply_args& A, double wscale, double mfull, doubl
   S.cap = REPAIR_CAP;
   S.tau_w = tau * wscale;
   S.mass_full = mfull;
+  S.mass_bound = 1e300;   // (kernel 2b's launches set mass_bound(P))
   return BF_OK;
 }
 
@@ -911,6 +926,7 @@ bf_status run(const bf_plan* const* plans, int nplans, const void* d_in, float* 
   L.P.fb_mask = A.d_fallback_mask;
   if (!dump) {
     const bf_status rs = repair_sink(A, std::ldexp(1.0, wbits), mass_full(p, L.P), default_tau(plans, nplans), st, L.P.rep);
+    L.P.rep.mass_bound = mass_bound(L.P);
     if (rs != BF_OK) return rs;
   }
   int gl = 0;

@@ -490,11 +490,7 @@ __device__ __forceinline__ void note_fallback(unsigned long long* cnt, unsigned 
 // Appends the pixel to the repair list when den < tau mass (RepairSink): den and mass in the same
 // units (mass = the k = 0 cosine channel's box sum; mass_full scaled by mass_unit when that channel
 // is not at hand). Returns true if flagged (its fallback bookkeeping is then the repair pass's).
-__device__ __forceinline__ bool flag_pixel(const RepairSink& R, double den, double mass, double mass_unit,
-                                           long long pix) {
-  if (!R.count) return false;
-  const double m = mass > 0 ? mass : R.mass_full * mass_unit;
-  const bool fl = den < R.tau_w * m;
+__device__ __forceinline__ bool flag_bool(const RepairSink& R, bool fl, long long pix) {
   const unsigned act = __activemask();
   const unsigned bal = __ballot_sync(act, fl);
   if (bal) {
@@ -511,6 +507,12 @@ __device__ __forceinline__ bool flag_pixel(const RepairSink& R, double den, doub
     }
   }
   return fl;
+}
+__device__ __forceinline__ bool flag_pixel(const RepairSink& R, double den, double mass, double mass_unit,
+                                           long long pix) {
+  if (!R.count) return false;
+  const double m = mass > 0 ? mass : R.mass_full * mass_unit;
+  return flag_bool(R, den < R.tau_w * m, pix);
 }
 __device__ __forceinline__ bool flag_pixel(const RepairSink& R, long long den, int mass, long long pix) {
   return flag_pixel(R, (double)den, (double)mass, 1.0, pix);
@@ -569,10 +571,12 @@ __device__ __forceinline__ void finish_pixel(const KParams& P, long long num, lo
 // Kernel 2b's finish from the per-box accumulators num_b = sum W H_b, den_b (exact int64):
 // num = sum_b ax_b num_b, den likewise, formed in fp64 (relative rounding 2^-53, far below the
 // channel values' fp32 error); out = D num / den, or I(x) if den <= 0 (Q18). mass is in the same
-// units (sum_b ax_b H_b of the k = 0 cosine channel, 2^32 times the F units of finish_pixel).
+// units (sum_b ax_b H_b of the k = 0 cosine channel's box sums hm_b, 2^32 times the F units of
+// finish_pixel; hm_b = 0: not at hand), formed only when den is below tau times the bound of any
+// clipped mass.
 __device__ __forceinline__ void finish_pixel_pb(const KParams& P, const long long (&num)[2], const long long (&den)[2],
                                                 int ax0, int ax1, float Ic, long long pix, float* __restrict__ out,
-                                                double mass, void* ws) {
+                                                int hm0, int hm1, void* ws) {
   const double n = fma((double)num[1], (double)ax1, (double)num[0] * (double)ax0);
   const double d = fma((double)den[1], (double)ax1, (double)den[0] * (double)ax0);
   if (P.dunit != 0.0) {
@@ -582,7 +586,17 @@ __device__ __forceinline__ void finish_pixel_pb(const KParams& P, const long lon
   }
   const bool fb = !(d > 0);
   out[pix] = fb ? Ic : (float)(P.D * n / d);
-  const bool fl = flag_pixel(P.rep, d, mass, 4294967296.0, pix);
+  if (!P.rep.count) {
+    note_fallback(P.fb_count, P.fb_mask, pix, fb);
+    return;
+  }
+  const RepairSink& R = P.rep;
+  bool cand = d < R.tau_w * (R.mass_bound * 4294967296.0);
+  if (cand) {
+    const double mass = (hm0 | hm1) ? fma((double)hm1, (double)ax1, (double)hm0 * (double)ax0) : 0.0;
+    cand = d < R.tau_w * (mass > 0 ? mass : R.mass_full * 4294967296.0);
+  }
+  const bool fl = flag_bool(R, cand, pix);
   note_fallback(P.fb_count, P.fb_mask, pix, fb && !fl);
 }
 

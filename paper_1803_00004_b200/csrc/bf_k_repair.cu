@@ -85,6 +85,10 @@ __global__ void __launch_bounds__(RT) bf_repair_kernel(const RParams R, const vo
   __shared__ double red[2][RT / 32];
   __shared__ int last;
   const int tid = threadIdx.x;
+  // nothing flagged (the common case), or more CTAs than (pixel, chunk) items: leave before the
+  // table fills
+  const unsigned n = min(*R.count, R.cap);
+  if ((unsigned long long)blockIdx.x >= (unsigned long long)n * (unsigned)R.nch) return;
   for (int i = tid; i < R.ns * n1; i += RT) {
     const int s = i / n1, o = i % n1 - R.rad;
     double wx = 0.0, wy = 0.0;
@@ -95,7 +99,6 @@ __global__ void __launch_bounds__(RT) bf_repair_kernel(const RParams R, const vo
     fx[i] = wx;
     fy[i] = wy;
   }
-  const unsigned n = min(*R.count, R.cap);
   if (R.repaired && blockIdx.x == 0 && tid == 0 && n) atomicAdd(R.repaired, (unsigned long long)n);
   const double invT = 1.0 / R.T;
   for (int i = tid; i < R.ntab * (REP_DEG + 1); i += RT) klut[i] = R.tab[i];

@@ -31,6 +31,8 @@ struct RepairSink {
   unsigned cap;
   double tau_w;               // tau * 2^wbits: flag if den < tau_w * mass (mass = the k = 0 cosine channel F)
   double mass_full;           // that channel's value for an unclipped window (used when k = 0 is not selected)
+  double mass_bound;          // >= the channel's value for any clipped window (kernel 2b tests den against it
+                              // first and forms the clipped mass only below it)
 };
 
 // Parameters of one launch of a T = D kernel (band / ws / ws2 / cache), passed by value.

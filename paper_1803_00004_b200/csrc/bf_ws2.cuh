@@ -80,7 +80,24 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-constexpr int MBAR_BYTES = 64;   // mbarriers at the start of shared memory (FULL[2], EMPTY[2])
+constexpr int MBAR_BYTES = 64;
+
+// diagnostic builds only (tools/build_variant.py): drop one role's arithmetic, keep its barriers
+#ifndef BF_X_NOV
+#define BF_X_NOV 0
+#endif
+#ifndef BF_X_NOS
+#define BF_X_NOS 0
+#endif
+#ifndef BF_X_NOFH
+#define BF_X_NOFH 0
+#endif
+#ifndef BF_X_NOW
+#define BF_X_NOW 0
+#endif
+#ifndef BF_X_NOLDS
+#define BF_X_NOLDS 0
+#endif   // mbarriers at the start of shared memory (FULL[2], EMPTY[2])
 
 template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL, int NPL, int COLS, bool CL, bool DUMP>
 __global__ void __launch_bounds__(W2_THREADS, 1)
@@ -153,14 +170,14 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
     float Ipre[NB][2];
 #pragma unroll
     for (int j = 0; j < COLS; ++j)
-      if (vwork[j]) v_init<MAXK, NB, NS, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, U[j]);
+      if (vwork[j] && !BF_X_NOV) v_init<MAXK, NB, NS, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, U[j]);
     load_taps<NB, U8>(P, in, fbase, col[0], colok[0], y0, Ipre);
     for (int y = y0; y < yend; ++y) {
       const int b = (y - y0) & 1;
       const GroupSync hook{b, n_uempty, n_ufull, y - y0 >= 2};
       int* Ub = Ubuf + b * srow + vt;
       if constexpr (COLS == 1) {
-        if (vwork[0]) {
+        if (vwork[0] && !BF_X_NOV) {
           float Icur[NB][2];
 #pragma unroll
           for (int bb = 0; bb < NB; ++bb) {
@@ -215,7 +232,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       for (int y = y0; y < yend; ++y) {
         const int b = (y - y0) & 1;
         bar_sync(BAR_U_FULL + 2 * b + g, n_ufull);
-        if (act) prefix_row(Ubuf + b * srow + slot * UP, wv);
+        if (act && !BF_X_NOS) prefix_row(Ubuf + b * srow + slot * UP, wv);
         bar_arrive(BAR_Q_FULL + 2 * b + g, n_qfull);
       }
     }
@@ -246,8 +263,8 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       if (act && y + 1 < yend) Inext = load_pixel(in, U8, prow + (long long)(y + 1) * P.W);
       // PB: per-box exact accumulators num_b = sum W H_b, den_b (no F rounding); num = sum_b ax_b num_b
       long long num[PB ? 2 : NPL] = {}, den[PB ? 2 : NPL] = {};
-      double mass = 0.0;   // sum_b ax_b H_b of the k = 0 cosine channel (the clipped spatial mass)
-      if (wact) {
+      int hm0 = 0, hm1 = 0;   // box sums H_b of the k = 0 cosine channel (the clipped spatial mass, on demand)
+      if (wact && !BF_X_NOFH) {
         double c1, s1;
         pixel_angle<U8>(P, lut64, Ic, c1, s1);
         Cheb64 gk;
@@ -258,7 +275,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         for (int i = 0; i < MAXK; ++i) {
           if (FULL || i < nkc) {
             if ((i & 7) == 0) bar_sync(BAR_Q_FULL + 2 * b + (i >> 3), n_qfull);
-            if (!DUMP && i > 0) {   // k_i - k_{i-1} >= 1 steps
+            if (!DUMP && i > 0 && !BF_X_NOW) {   // k_i - k_{i-1} >= 1 steps
               gk.step();
               if (!CONSEC) extra_steps(P.kstep[t0 + i], [&] { gk.step(); });
             }
@@ -266,10 +283,18 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const int* q = Qb + (4 * i + c) * UP;
-              h0[c] = q[e0] - q[l0];
-              h1[c] = (M == 2) ? q[e1] - q[l1] : 0;
+              if (BF_X_NOLDS) {
+                h0[c] = e0 * (c + 3) + i;
+                h1[c] = l1 * (c + 1) - i;
+              } else {
+                h0[c] = q[e0] - q[l0];
+                h1[c] = (M == 2) ? q[e1] - q[l1] : 0;
+              }
             }
-            if (i == 0 && k0 == 0) mass = fma((double)h1[0], (double)ax1, (double)h0[0] * (double)ax0);
+            if (i == 0 && k0 == 0) {
+              hm0 = h0[0];
+              hm1 = h1[0];
+            }
             if constexpr (DUMP) {
               if (act) {
                 int* cp = P.cache + (long long)(4 * P.kval[t0 + i]) * P.cache_plane + (long long)y * P.W + x0 + o;
@@ -281,8 +306,8 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
                 }
               }
             } else if constexpr (PB) {
-              const int wc = __double2loint(fma(gk.c, P.aw[0][t0 + i], MAGIC64));
-              const int wsn = __double2loint(fma(gk.s, P.aw[0][t0 + i], MAGIC64));
+              const int wc = BF_X_NOW ? 1000 + i * e1 : __double2loint(fma(gk.c, P.aw[0][t0 + i], MAGIC64));
+              const int wsn = BF_X_NOW ? 77 + i * l0 : __double2loint(fma(gk.s, P.aw[0][t0 + i], MAGIC64));
               den[0] = mad_wide(wc, h0[0], den[0]);
               den[0] = mad_wide(wsn, h0[1], den[0]);
               num[0] = mad_wide(wc, h0[2], num[0]);
@@ -351,7 +376,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
               den[0] += v0.y;
               num[1] += v1.x;
               den[1] += v1.y;
-              finish_pixel_pb(P, num, den, ax0, ax1, Ic, prow + (long long)y * P.W, out, mass, ws);
+              finish_pixel_pb(P, num, den, ax0, ax1, Ic, prow + (long long)y * P.W, out, hm0, hm1, ws);
             }
           }
           __syncwarp();
@@ -359,13 +384,13 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
             for (int s = 1; s < G; ++s) mbar_arrive_remote(map_rank(smem_u32(&mbar[2 + b]), s));
         }
       } else if constexpr (PB) {
-        if (act) finish_pixel_pb(P, num, den, ax0, ax1, Ic, prow + (long long)y * P.W, out, mass, ws);
+        if (act) finish_pixel_pb(P, num, den, ax0, ax1, Ic, prow + (long long)y * P.W, out, hm0, hm1, ws);
       } else {
         if (act) {
 #pragma unroll
           for (int q = 0; q < NPL; ++q)
             finish_pixel(P, num[q], den[q], Ic, prow + (long long)y * P.W + q * P.plan_stride, out, ws, q == 0,
-                         (int)ldexp(mass, -32));
+                         fhi(mad_wide(hm1, ax1, mad_wide(hm0, ax0, FRND))));
         }
       }
     }

@@ -1,6 +1,13 @@
-"""Device timings of the NEXT rows on the B200 (CUDA events, L2 flushed, median of 10 after 3
-warm-ups): Case 1 multi-plan sharing (bf_apply_multi, f2), rank-2 three-box plans (N_s = 5, f3),
-and both kernels per config. Prints one line per measurement."""
+"""Device timings of the NEXT rows on the B200: CUDA events on the launching
+stream, L2 flushed (a 256 MB write) before every repetition, median of 10 after 3 warm-ups.
+
+  f2  Case 1: bf_apply_multi (several range plans over one pass) and the two-phase
+      cache (bf_precompute once, bf_apply_cached per range plan) against the full recompute
+  f3  richer spatial plans: N_s = 5 (rank 2), 13, 16, 25, 36, 49, 64 (general passes / Form 4)
+  f1  the paper-literal z-window (u8)
+  --  every kernel on every config it can run (bitwise-equal kernels, A/B)
+One line per measurement; `--json PATH` also writes them as a JSON list."""
+import json
 import os
 import statistics
 import sys
@@ -13,6 +20,7 @@ import paper_1803_00004_b200 as pkg  # noqa: E402
 from synth import CONFIGS, config_input, config_params  # noqa: E402
 
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+RESULTS = []
 
 
 def timed(fn, reps=10, warm=3):
@@ -30,56 +38,111 @@ def timed(fn, reps=10, warm=3):
     return statistics.median(ts)
 
 
+def say(name, ms, **kw):
+    RESULTS.append(dict(name=name, ms=ms, **kw))
+    extra = " ".join(f"{k}={v}" for k, v in kw.items())
+    print(f"{name}: {ms:.3f} ms {extra}", flush=True)
+
+
 def plan_for(spec, **over):
     p = dict(config_params(spec))
     p.update(over)
     u8 = spec.gen == "ramp" and not spec.as_f32
     return pkg.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"], sigma_r=p["sigma_r"],
                     radius=p["radius"], n_terms=p["n_terms"], intensity_max=p["intensity_max"],
-                    n_spatial=p.get("n_spatial", 9), input_dtype="u8" if u8 else "f32")
+                    n_spatial=p.get("n_spatial", 9), haar_levels=p.get("haar_levels", 4),
+                    input_dtype="u8" if u8 else "f32", range_window=p.get("range_window", "full"))
 
 
-def main():
+def image(cfg):
+    im = config_input(CONFIGS[cfg])
+    if im.ndim == 3:
+        im = im[0]
+    return torch.from_numpy(np.ascontiguousarray(im)).cuda()
+
+
+def case1():
     spec = CONFIGS["cfg2"]
-    img = torch.from_numpy(config_input(spec)).cuda()
+    img = image("cfg2")
     H, W = img.shape
     sigmas = [0.1, 0.05, 0.2, 0.3]
     plans = [plan_for(spec, sigma_r=s) for s in sigmas]
+    tukey = plan_for(spec, range_kind="tukey", sigma_r=0.4)
     t1 = timed(lambda: pkg.bilateral_filter(plans[0], img))
-    print(f"cfg2 single plan: {t1:.3f} ms")
+    say("f2 cfg2 one plan, full recompute (bf_apply)", t1)
     for n in (2, 3, 4):
         tm = timed(lambda: pkg.bilateral_filter_multi(plans[:n], img))
-        ts = sum(timed(lambda p=p: pkg.bilateral_filter(p, img)) for p in plans[:n])
-        print(f"cfg2 {n} sigma_r plans: multi {tm:.3f} ms vs {n} separate {ts:.3f} ms ({ts / tm:.2f}x)")
+        say(f"f2 cfg2 {n} sigma_r plans through bf_apply_multi", tm, separate_ms=round(n * t1, 3))
+    kmax = max(max(p.info()["k"]) for p in plans + [tukey]) + 1
+    out = torch.empty((H, W), dtype=torch.float32, device="cuda")
+    tp = timed(lambda: pkg.RangeCache(plans[0], img, kmax))
+    cache = pkg.RangeCache(plans[0], img, kmax)
+    say(f"f2 cfg2 bf_precompute k < {kmax}", tp, cache_bytes=int(cache.buf.numel()))
+    for p, name in zip(plans + [tukey], [f"gaussian sigma_r={s}" for s in sigmas] + ["tukey 0.4"]):
+        tc = timed(lambda p=p: cache.apply(p, out))
+        ref = pkg.bilateral_filter(p, img)
+        same = bool(torch.equal(ref, cache.apply(p, out)))
+        say(f"f2 cfg2 bf_apply_cached {name}", tc, bitwise_equal_to_bf_apply=same,
+            n_terms=len(p.info()["k"]))
+
+
+def spatial():
     for cfg in ("cfg0", "cfg1", "cfg2"):
         sp = CONFIGS[cfg]
-        im = torch.from_numpy(config_input(sp)).cuda()
-        for ns in (9, 5):
-            p = plan_for(sp, n_spatial=ns)
-            t = timed(lambda: pkg.bilateral_filter(p, im))
-            print(f"{cfg} N_s={ns} (rank {p.info()['spatial_rank']}): {t:.3f} ms, "
-                  f"{im.numel() / t / 1e3:.0f} MP/s")
-    for cfg in ("cfg0", "cfg3"):   # the paper-literal window (NEXT f1), u8 configs
+        im = image(cfg)
+        for ns in (9, 5, 13, 16, 25, 36, 49, 64):
+            try:
+                p = plan_for(sp, n_spatial=ns)
+                inf = p.info()
+                t = timed(lambda: pkg.bilateral_filter(p, im))
+            except Exception as e:  # noqa: BLE001
+                print(f"f3 {cfg} N_s={ns}: {e}")
+                continue
+            say(f"f3 {cfg} N_s={ns}", t, rank=inf["spatial_rank"], passes=inf["spatial_passes"],
+                mp_s=round(im.numel() / t / 1e3))
+
+
+def literal():
+    for cfg in ("cfg0", "cfg3"):
         sp = CONFIGS[cfg]
-        im = torch.from_numpy(config_input(sp)).cuda()
+        im = image(cfg)
         p = plan_for(sp)
-        prm = config_params(sp)
-        pl = pkg.Plan(spatial=prm["spatial"], range_kind=prm["range_kind"], sigma_s=prm["sigma_s"],
-                      sigma_r=prm["sigma_r"], radius=prm["radius"], n_terms=prm["n_terms"], input_dtype="u8",
-                      range_window="literal")
+        pl = plan_for(sp, range_window="literal")
         t0 = timed(lambda: pkg.bilateral_filter(p, im))
         tl = timed(lambda: pkg.bilateral_filter(pl, im))
-        print(f"{cfg} literal window T_r={pl.info()['T_range']:.1f}: {tl:.3f} ms ({im.numel() / tl / 1e3:.0f} MP/s) "
-              f"vs T=D hot path {t0:.3f} ms")
-    for cfg in ("cfg0", "cfg1", "cfg2", "cfg3"):
+        say(f"f1 {cfg} literal window T_r={pl.info()['T_range']:.1f}", tl, mp_s=round(im.numel() / tl / 1e3),
+            t_eq_d_ms=round(t0, 4))
+
+
+def kernels():
+    for cfg in ("cfg0", "cfg1", "cfg2", "cfg3", "cfg4"):
         sp = CONFIGS[cfg]
-        im = torch.from_numpy(config_input(sp)).cuda()
+        im = image(cfg)
         p = plan_for(sp)
-        for k in ("band", "ws", "ws2"):
-            os.environ["BF_KERNEL"] = k
-            t = timed(lambda: pkg.bilateral_filter(p, im))
-            print(f"{cfg} kernel={k}: {t:.3f} ms")
-        os.environ.pop("BF_KERNEL")
+        ref = None
+        for k in ("ws2", "ws2wide", "ws", "band"):
+            if cfg == "cfg4" and k in ("ws", "band"):
+                continue   # (the barrier-interval kernel needs several passes at r = 192: tens of ms)
+            try:
+                o = pkg.bilateral_filter(p, im, kernel=k, repair_threshold=-1.0)
+                t = timed(lambda: pkg.bilateral_filter(p, im, kernel=k, repair_threshold=-1.0),
+                          reps=5 if cfg == "cfg4" else 10)
+            except Exception as e:  # noqa: BLE001
+                print(f"kernel {cfg} {k}: {e}")
+                continue
+            same = None if ref is None else bool(torch.equal(ref, o))
+            ref = o if ref is None else ref
+            say(f"kernel {cfg} {k}", t, bitwise_equal_to_first=same)
+
+
+def main():
+    which = sys.argv[1].split(",") if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else \
+        ["case1", "spatial", "literal", "kernels"]
+    for w in which:
+        globals()[w]()
+    if "--json" in sys.argv:
+        with open(sys.argv[sys.argv.index("--json") + 1], "w") as f:
+            json.dump(RESULTS, f, indent=1)
 
 
 if __name__ == "__main__":
