@@ -277,8 +277,8 @@ BF_API bf_status bf_apply_launches(const bf_plan* plan, int H, int W, int* n_lau
  * n_frames = 1): kernel name (a static string owned by the library), threads per CTA, grid
  * (strips x bands x frames), output tile (columns per strip, rows per band), dynamic shared
  * memory per CTA and the number of launches (passes). Pure host computation, no device work;
- * the kernel choice and band height follow the same rules (and BF_KERNEL / BF_TH tuning
- * variables) as the apply call. Errors as bf_apply_launches. */
+ * the kernel choice and band height follow the same rules (bf_apply_args.kernel / band_rows)
+ * as the apply call. Errors as bf_apply_launches. */
 typedef struct bf_launch_config {
   int n_launches;
   const char* kernel;
@@ -299,17 +299,21 @@ BF_API bf_status bf_apply_config(const bf_plan* plan, int n_frames, int H, int W
 /*
  * Case 1 of the paper's pre-computation (NEXT f2), the paper's two phases:
  * bf_precompute runs once per image and stores the box-filtered channels of the frequencies
- * k = 0 .. k_count-1 (4 int32 planes per k: S(g^c_k), S(g^s_k), S(G^c_k), S(G^s_k) of
- * eq:numerator_2D_box_N_terms; with T_{r_i} = D they do not depend on the range kernel,
- * P:1205) in the caller's device buffer d_cache (bf_cache_size bytes; layout plane
- * 4k + c of H*W int32, row-major). bf_apply_cached then evaluates any range plan whose selected
- * k all lie below k_count and whose spatial plan, D and input dtype equal the precompute plan's,
- * as one combine-only pass that reads the cache and the input (HBM-bound); its output equals
- * bf_apply's bitwise. Both are asynchronous on `stream`, allocate nothing and are graph
- * capturable. desc (host memory, filled by bf_precompute) carries what bf_apply_cached checks.
+ * k = 0 .. k_count-1 (S(g^c_k), S(g^s_k), S(G^c_k), S(G^s_k) of eq:numerator_2D_box_N_terms,
+ * P:481-493; with T_{r_i} = D they do not depend on the range kernel) in the
+ * caller's device buffer d_cache (bf_cache_size bytes, 16-byte aligned; layout: plane k of H*W
+ * row-major 16-byte entries, entry = the four channels as int32 in that order, each the
+ * box-weighted sum F = round(sum_b ax_b H_b / 2^32) of the exact box sums H_b). bf_apply_cached
+ * then evaluates any range plan whose selected k all lie below k_count and whose spatial plan, D
+ * and input dtype equal the precompute plan's, as one combine-only pass that reads the cache and
+ * the input (HBM-bound: 16 B per selected term per pixel). Its output equals bf_apply's to the
+ * rounding of F (bf_apply's default kernel keeps the per-box sums exact; the kernels that form F,
+ * BF_KERNEL_WS / BF_KERNEL_BAND, agree with it bitwise). Both are asynchronous on `stream`,
+ * allocate nothing and are graph capturable. desc (host memory, filled by bf_precompute) carries
+ * what bf_apply_cached checks.
  * Errors: BF_ERR_INVALID_ARG for NULL pointers, sizes, k_count outside [1, BF_MAX_TERMS], a too
- * small cache, or a plan that does not match desc; BF_ERR_UNSUPPORTED for literal plans and
- * spatial plans other than separable with at most two boxes per axis.
+ * small or misaligned cache, or a plan that does not match desc; BF_ERR_UNSUPPORTED for literal
+ * plans and spatial plans other than separable with at most two boxes per axis.
  */
 typedef struct {
   int k_count, H, W, input_dtype;

@@ -1074,7 +1074,8 @@ extern "C" bf_status bf_precompute(const bf_plan* plan, int k_count, const void*
   size_t need = 0;
   bf_status s = bf_cache_size(plan, k_count, H, W, &need);
   if (s != BF_OK) return s;
-  if (!d_in || !d_cache || !desc || cache_bytes < need) return BF_ERR_INVALID_ARG;
+  if (!d_in || !d_cache || !desc || cache_bytes < need || (reinterpret_cast<uintptr_t>(d_cache) & 15))
+    return BF_ERR_INVALID_ARG;
   if (plan->literal) return BF_ERR_UNSUPPORTED;
   int rlo, rhi;
   const int form = plan_form(plan, rlo, rhi);
@@ -1115,7 +1116,9 @@ extern "C" bf_status bf_precompute(const bf_plan* plan, int k_count, const void*
 
 extern "C" bf_status bf_apply_cached(const bf_plan* plan, const bf_cache_desc* desc, const void* d_cache,
                                      const void* d_in, float* d_out, bf_stream stream, const bf_apply_args* args) {
-  if (!plan || !desc || !d_cache || !d_in || !d_out || (const void*)d_out == d_in) return BF_ERR_INVALID_ARG;
+  if (!plan || !desc || !d_cache || !d_in || !d_out || (const void*)d_out == d_in ||
+      (reinterpret_cast<uintptr_t>(d_cache) & 15))
+    return BF_ERR_INVALID_ARG;
   if (plan->literal) return BF_ERR_UNSUPPORTED;
   if (desc->H <= 0 || desc->W <= 0 || plan->input_dtype != desc->input_dtype || plan->D != desc->intensity_max ||
       spatial_key(plan) != desc->spatial_key)
@@ -1132,11 +1135,14 @@ extern "C" bf_status bf_apply_cached(const bf_plan* plan, const bf_cache_desc* d
   C.plane = (long long)desc->H * desc->W;
   C.nk = plan->n_k;
   const int wbits = combine_bits(&plan, 1);
+  C.mass_i = -1;
   for (int i = 0; i < plan->n_k; ++i) {
     C.ch[i] = plan->k[i];
     C.kval[i] = plan->k[i];
+    C.kstep[i] = i ? plan->k[i] - plan->k[i - 1] : 0;
     C.aw[i] = std::ldexp(plan->a[i], wbits);
-  }
+    if (plan->k[i] == 0) C.mass_i = i;
+  }   // (kstep / aw beyond n_k stay 0: the padding of the last chunk)
   C.invD = 1.0 / plan->D;
   C.D = plan->D;
   C.u8 = plan->input_dtype == BF_IN_U8;
@@ -1148,7 +1154,7 @@ extern "C" bf_status bf_apply_cached(const bf_plan* plan, const bf_cache_desc* d
   quantise(plan, Q);
   const bf_status rs = repair_sink(A, std::ldexp(1.0, wbits), mass_full(plan, Q), default_tau(&plan, 1), st, C.rep);
   if (rs != BF_OK) return rs;
-  cudaError_t err = launch_cached(C, static_cast<const int*>(d_cache), d_in, d_out, st);
+  cudaError_t err = launch_cached(C, static_cast<const int4*>(d_cache), d_in, d_out, st);
   if (err == cudaSuccess && C.rep.count) {
     RParams Rp;
     repair_params(&plan, 1, 1, desc->H, desc->W, A, C.rep, Rp);

@@ -69,7 +69,7 @@ struct KParams {
   unsigned long long* fb_count;    // optional: += pixels that took the den <= 0 fallback (Q18)
   unsigned char* fb_mask;          // optional: 1 where the pixel took the fallback, else 0
   int* cache;                 // bf_precompute: box-filtered channel planes F[ch][y][x] (int32)
-  long long cache_plane;      // elements per cache plane (H * W)
+  long long cache_plane;      // int4 entries per cache plane (H * W)
   RepairSink rep;             // ill-conditioned pixels for the fp64 repair pass
   double uscale;              // absolute value of one unit of F (times 2^wbits): wxmax wymax 2^-(abits-32+q-ush)
   double dunit;               // general plans: uscale * 2^-wbits, num / den accumulated in fp64 (0 = off)
@@ -137,18 +137,20 @@ cudaError_t launch_literal(const LParams& L, const unsigned char* in, float* out
 // Case 1 cache (NEXT f2): combine-only pass over precomputed box-filtered channels.
 struct CParams {
   int H, W;
-  long long plane;            // elements per channel plane
+  long long plane;            // int4 entries per cache plane (H * W)
   int nk;                     // terms combined
-  int ch[BF_MAX_TERMS];       // cache channel-quad index of term i (its k's slot in the cache)
+  int ch[BF_MAX_TERMS];       // cache plane of term i (its k)
   int kval[BF_MAX_TERMS];
-  double aw[BF_MAX_TERMS];    // a_k * 2^wbits
+  int kstep[BF_MAX_TERMS + 8];   // k_i - k_{i-1} (i >= 1); 0 in the padding
+  double aw[BF_MAX_TERMS + 8];   // a_k * 2^wbits; 0 in the padding (the kernel runs whole chunks)
+  int mass_i;                 // index of the k = 0 term, or -1
   double invD, D;
   int u8;
   unsigned long long* fb_count;
   unsigned char* fb_mask;
   RepairSink rep;
 };
-cudaError_t launch_cached(const CParams& C, const int* cache, const void* in, float* out, cudaStream_t st);
+cudaError_t launch_cached(const CParams& C, const int4* cache, const void* in, float* out, cudaStream_t st);
 
 // fp64 repair of the flagged pixels (bf_k_repair.cu).
 constexpr int REP_DEG = 13, REP_TAB = 2048;

@@ -297,13 +297,17 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
             }
             if constexpr (DUMP) {
               if (act) {
-                int* cp = P.cache + (long long)(4 * P.kval[t0 + i]) * P.cache_plane + (long long)y * P.W + x0 + o;
+                // cache plane k: the pixel's four channels as one 16-byte entry
+                int4* cp = reinterpret_cast<int4*>(P.cache) + (long long)P.kval[t0 + i] * P.cache_plane +
+                           (long long)y * P.W + x0 + o;
+                int F[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                   long long f = mad_wide(h0[c], ax0, FRND);
                   if (M == 2) f = mad_wide(h1[c], ax1, f);
-                  cp[c * P.cache_plane] = fhi(f);
+                  F[c] = fhi(f);
                 }
+                __stcs(cp, make_int4(F[0], F[1], F[2], F[3]));
               }
             } else if constexpr (PB) {
               const int wc = BF_X_NOW ? 1000 + i * e1 : __double2loint(fma(gk.c, P.aw[0][t0 + i], MAGIC64));
