@@ -285,9 +285,6 @@ template <> struct Form<5> { static constexpr int NS = 2, NBY = 2, NBX = 1; };  
 
 // ------------------------------------------------------------------ the steps of a row
 
-// Vertical state at row y0 - 1 of the terms [t0, t0 + nk): U = urnd + sum over the rows v of the
-// vertical boxes of the quantised channels (every tap's scale carries the box weight, nested
-// boxes add up).
 // (cos, sin)(pi i / D) of a u8 level by direct evaluation: the values the Case 2 LUT holds
 __device__ __forceinline__ float2 u8_direct(float I, double invD) {
   double s, c;
@@ -295,55 +292,73 @@ __device__ __forceinline__ float2 u8_direct(float I, double invD) {
   return make_float2((float)c, (float)s);
 }
 
+// sum of a packed pair of quantised values, q(lo) + q(hi) (both MAGIC biases removed)
+__device__ __forceinline__ int sum_bits(u64 v) {
+  int a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(a), "=r"(b) : "l"(v));
+  return a + b - 2 * MAGIC_BITS;
+}
+
+// Vertical state at row y0 - 1 of the terms [t0, t0 + nk): U = urnd + sum over the rows v of the
+// vertical boxes of the quantised channels (every tap's scale carries the box weight, nested
+// boxes add up). Two rows per step on packed lanes (FFMA2 / FMUL2), each lane bit-identical to the tap
+// arithmetic of v_row (same base angle, recurrence and quantisation), so the state equals the one
+// the sliding enter / leave taps would build exactly; a row outside the window of box b (or the
+// image, or the odd last row) gets scale 0, which quantises to exactly 0.
 template <int MAXK, int NB, int NS, bool U8, bool CONSEC, bool FULL, bool POW = false, bool DIRECT = false>
 __device__ __forceinline__ void v_init(const KParams& P, const void* __restrict__ in, const float2* lut,
                                        long long fbase, int col, bool colok, int y0, int t0, int nk,
                                        int (&U)[NS * 4 * MAXK]) {
 #pragma unroll
   for (int ch = 0; ch < NS * 4 * MAXK; ++ch) U[ch] = P.urnd;
-  for (int v = P.vmin; v <= P.vmax; ++v) {
-    const int row = y0 - 1 + v;
-    const bool ok = colok && row >= 0 && row < P.H;
-    const float I = ok ? load_pixel(in, U8, fbase + (long long)row * P.W + col) : 0.f;
-    float c1, s1;
+  const u64 MM = pk(MAGIC, MAGIC);
+  const int k0 = P.kval[t0];
+  for (int v = P.vmin; v <= P.vmax; v += 2) {
+    const int ra = y0 - 1 + v, rb = ra + 1;
+    const bool oka = colok && ra >= 0 && ra < P.H;
+    const bool okb = colok && v + 1 <= P.vmax && rb >= 0 && rb < P.H;
+    const float Ia = oka ? load_pixel(in, U8, fbase + (long long)ra * P.W + col) : 0.f;
+    const float Ib = okb ? load_pixel(in, U8, fbase + (long long)rb * P.W + col) : 0.f;
+    Rot2 g2;
     if (U8) {
-      const float2 t = DIRECT ? u8_direct(I, P.invD) : lut[(int)I];
-      c1 = t.x;
-      s1 = t.y;
+      const float2 ta = DIRECT ? u8_direct(Ia, P.invD) : lut[(int)Ia];
+      const float2 tb = DIRECT ? u8_direct(Ib, P.invD) : lut[(int)Ib];
+      g2.init(ta.x, ta.y, tb.x, tb.y);
     } else {
-      base_angle_f32(I, P, c1, s1);
+      u64 c1, s1;
+      base_angle_f32x2(Ia, Ib, P, c1, s1);
+      g2.init2(c1, s1);
     }
-    float scb[NS][NB], scIb[NS][NB];
+    u64 QS[NS][NB], QI[NS][NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      const bool in_b = ok && (b < P.nby) && v >= P.vlo[b] && v <= P.vhi[b];
+      const bool ina = oka && (b < P.nby) && v >= P.vlo[b] && v <= P.vhi[b];
+      const bool inb = okb && (b < P.nby) && v + 1 >= P.vlo[b] && v + 1 <= P.vhi[b];
 #pragma unroll
       for (int t = 0; t < NS; ++t) {
-        scb[t][b] = in_b ? P.qs[t][b] : 0.f;
-        scIb[t][b] = in_b ? P.qsD[t][b] * I : 0.f;
+        QS[t][b] = pk(ina ? P.qs[t][b] : 0.f, inb ? P.qs[t][b] : 0.f);
+        QI[t][b] = pk(ina ? P.qsD[t][b] * Ia : 0.f, inb ? P.qsD[t][b] * Ib : 0.f);
       }
     }
-    float gc = 1.f, gs = 0.f;
-    if (POW) rot1_start(gc, gs, c1, s1, P.kval[t0]);
+    if (POW) g2.start(k0);
     else
-      for (int j = 0; j < P.kval[t0]; ++j) rot1(gc, gs, c1, s1);
+      for (int j = 0; j < k0; ++j) g2.step();
 #pragma unroll
     for (int i = 0; i < MAXK; ++i) {
       if (FULL || i < nk) {
         if (i > 0) {
-          if (CONSEC) rot1(gc, gs, c1, s1);
-          else
-            for (int j = 0; j < P.kstep[t0 + i]; ++j) rot1(gc, gs, c1, s1);   // (init rows only)
+          g2.step();
+          if (!CONSEC) extra_steps(P.kstep[t0 + i], [&] { g2.step(); });
         }
 #pragma unroll
         for (int t = 0; t < NS; ++t)
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             int* Ut = U + t * 4 * MAXK;
-            Ut[4 * i + 0] += quant(gc, scb[t][b]);
-            Ut[4 * i + 1] += quant(gs, scb[t][b]);
-            Ut[4 * i + 2] += quant(gc, scIb[t][b]);
-            Ut[4 * i + 3] += quant(gs, scIb[t][b]);
+            Ut[4 * i + 0] += sum_bits(fma2(g2.C, QS[t][b], MM));
+            Ut[4 * i + 1] += sum_bits(fma2(g2.S, QS[t][b], MM));
+            Ut[4 * i + 2] += sum_bits(fma2(g2.C, QI[t][b], MM));
+            Ut[4 * i + 3] += sum_bits(fma2(g2.S, QI[t][b], MM));
           }
       }
     }
