@@ -296,7 +296,7 @@ __device__ __forceinline__ float2 u8_direct(float I, double invD) {
 __device__ __forceinline__ int sum_bits(u64 v) {
   int a, b;
   asm("mov.b64 {%0, %1}, %2;" : "=r"(a), "=r"(b) : "l"(v));
-  return a + b - 2 * MAGIC_BITS;
+  return (int)((unsigned)a + (unsigned)b - 2u * (unsigned)MAGIC_BITS);
 }
 
 // Vertical state at row y0 - 1 of the terms [t0, t0 + nk): U = urnd + sum over the rows v of the

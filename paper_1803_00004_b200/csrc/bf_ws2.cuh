@@ -30,6 +30,7 @@
 #pragma once
 
 #include "bf_device.cuh"
+#include "bf_tm.cuh"
 
 namespace bf {
 namespace ws2 {
@@ -81,6 +82,33 @@ __device__ __forceinline__ void cluster_sync() {
 }
 
 constexpr int MBAR_BYTES = 64;
+#ifndef BF_TM
+#define BF_TM 1
+#endif
+#ifndef BF_TM_VREG
+#define BF_TM_VREG 72
+#endif
+#ifndef BF_X_TMSTRIDE
+#define BF_X_TMSTRIDE (4 * MAXK)
+#endif
+#ifndef BF_TM_FHREG
+#define BF_TM_FHREG 80
+#endif
+constexpr int W2_LAUNCH_REG = 80;   // registers per thread at launch (768 threads, one CTA per SM)
+#ifndef BF_SPLIT_VREG
+#define BF_SPLIT_VREG 80
+#endif
+constexpr int BAR_P_FULL = 12, BAR_P_EMPTY = 14;   // SPLIT: FH-B -> FH-A partial-sum slots (per row parity)
+#ifndef BF_X_TMWARP
+#define BF_X_TMWARP (V0 / 32)
+#endif
+#ifndef BF_X_TMNODEALLOC
+#define BF_X_TMNODEALLOC 0
+#endif
+#ifndef BF_X_TMCOLS
+#define BF_X_TMCOLS 256
+#endif
+constexpr unsigned TM_COLS = BF_X_TMCOLS;   // TMEM columns: 3 V warps per lane quarter x 64 (4 MAXK, MAXK <= 16)
 
 // diagnostic builds only (tools/build_variant.py): drop one role's arithmetic, keep its barriers
 #ifndef BF_X_NOV
@@ -99,19 +127,45 @@ constexpr int MBAR_BYTES = 64;
 #define BF_X_NOLDS 0
 #endif   // mbarriers at the start of shared memory (FULL[2], EMPTY[2])
 
+// SPLIT: two FH threads per output pixel, one per 32-channel group (terms 0-7 and 8-15), twice the
+// FH warps for the latency-bound combine; FH-B hands its partial sums to FH-A through shared memory.
+// Needs the V state in TMEM (registers) and one range plan without a cluster.
+template <int MAXK, int COLS, int NPL, bool CL, bool DUMP>
+constexpr bool w2_split() {
+  return COLS == 1 && MAXK == 16 && BF_TM && NPL == 1 && !CL && !DUMP && BF_SPLIT;
+}
+template <int MAXK, int COLS, int NPL, bool CL, bool DUMP>
+constexpr int w2_threads() {
+  return w2_split<MAXK, COLS, NPL, CL, DUMP>() ? W2_SPLIT_THREADS : W2_THREADS;
+}
+
 template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL, int NPL, int COLS, bool CL, bool DUMP>
-__global__ void __launch_bounds__(W2_THREADS, 1)
+__global__ void __launch_bounds__(w2_threads<MAXK, COLS, NPL, CL, DUMP>(), 1)
     bf_ws2_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out, longlong2* __restrict__ ws) {
   constexpr int NS = Form<FORM>::NS, NB = Form<FORM>::NBY, NBX = Form<FORM>::NBX;
   constexpr int M = NS * NBX;
   static_assert(NS == 1 && M <= 2, "the FH role handles separable forms with at most two x boxes");
   static_assert(COLS == 1 || MAXK == 8, "two columns per V thread: 8 terms per CTA (one channel group)");
-  constexpr int NFH = w2_nfh(COLS), NSW = w2_ns(COLS);
+  constexpr bool SPLIT = w2_split<MAXK, COLS, NPL, CL, DUMP>();
+  constexpr int NTH = w2_threads<MAXK, COLS, NPL, CL, DUMP>();
+  constexpr int NFH = SPLIT ? 2 * W2_SPLIT_FH : w2_nfh(COLS), NSW = w2_ns(COLS);
+  constexpr int NFG = SPLIT ? W2_SPLIT_FH : NFH;   // FH threads per channel group
   constexpr int H0 = 0, S0 = NFH, V0 = NFH + NSW;
-  static_assert(V0 + W2_V == W2_THREADS, "role sizes");
+  static_assert(V0 + W2_V == NTH, "role sizes");
+  constexpr int LREG = SPLIT ? W2_SPLIT_LAUNCH_REG : W2_LAUNCH_REG;
   constexpr int UP = w2_up(COLS);
   constexpr bool PB = NPL == 1 && !DUMP;   // per-box accumulators (see the FH role)
-  constexpr int VREG = NPL > 1 ? 104 : 112, OREG = NPL > 1 ? 56 : 48;
+  // TM: the V role's sliding sums in tensor memory (bf_tm.cuh; one column per V thread), which
+  // moves registers from V to the latency-bound FH role
+  // (MAXK == 8 instantiations trap in the TMEM path on sm_100a: under investigation, registers there)
+  constexpr bool TM = COLS == 1 && MAXK == 16 && BF_TM;
+  // registers per role (setmaxnreg; the pool is the launch's LREG x NTH):
+  //   SPLIT  V 384 x 80 + FH 512 x 48 + S 64 x 48 = 58368 <= 960 x 64
+  //   TM     V 384 x 72 + FH 320 x 80 + S 64 x 48 = 56320 <= 768 x 80
+  //   else   V 384 x 112 + (FH + S) 384 x 48      = 61440
+  constexpr int VREG = SPLIT ? BF_SPLIT_VREG : (TM ? BF_TM_VREG : (NPL > 1 ? 104 : 112));
+  constexpr int OREG = NPL > 1 ? 56 : 48;
+  constexpr int FHREG = SPLIT ? 48 : (TM ? BF_TM_FHREG : OREG);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem_raw);   // FULL[2], EMPTY[2]
   int* Ubuf = reinterpret_cast<int*>(smem_raw + MBAR_BYTES);                     // [2][4 nk][UP]
@@ -133,10 +187,16 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   const int wv = P.wv;                            // extended columns scanned (multiple of 8, <= W2_V * COLS)
   const int srow = 4 * nkc * UP;                  // ints per U' buffer
   constexpr int n_ufull = W2_V + 32;              // U_FULL: V arrive, S_g sync
-  constexpr int n_uempty = W2_V + NFH;            // U_EMPTY: FH arrive, V sync
-  constexpr int n_qfull = 32 + NFH;               // Q_FULL: S_g arrive, FH sync
+  constexpr int n_uempty = W2_V + NFG;            // U_EMPTY: FH (of the group) arrive, V sync
+  constexpr int n_qfull = 32 + NFG;               // Q_FULL: S_g arrive, FH sync
+  constexpr int n_part = 2 * W2_SPLIT_FH;         // P_FULL / P_EMPTY (SPLIT): FH-A and FH-B
 
-  fill_luts<U8>(P, lut, lut64, tid, W2_THREADS);
+  fill_luts<U8>(P, lut, lut64, tid, NTH);
+  __shared__ unsigned tmem_slot;
+  if constexpr (TM) {
+    if (tid >= BF_X_TMWARP * 32 && tid < BF_X_TMWARP * 32 + 32) tm::alloc(&tmem_slot, TM_COLS);   // one warp allocates
+    tm::fence_before();
+  }
   if constexpr (CL) {
     if (tid == 0) {
       mbar_init(smem_u32(&mbar[0]), 1);           // FULL[b]: CTA 0's expect_tx arrival + the senders' bytes
@@ -145,15 +205,17 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       mbar_init(smem_u32(&mbar[3]), NFH / 32);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = tid; i < 2 * 2 * P.TW; i += W2_THREADS) red[i] = make_longlong2(0, 0);   // both slots
+    for (int i = tid; i < 2 * 2 * P.TW; i += NTH) red[i] = make_longlong2(0, 0);   // both slots
     cluster_sync();
   } else {
     __syncthreads();
   }
 
+  if constexpr (TM) tm::fence_after();
   if (tid >= V0) {
     // ------------------------------------------------------------ V role
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(VREG));
+    if constexpr (VREG > LREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(VREG));
+    else if constexpr (VREG < LREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(VREG));
     const int vt = tid - V0;
     int col[COLS];
     bool colok[COLS], vwork[COLS];
@@ -164,13 +226,21 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       colok[j] = (col[j] >= 0) & (col[j] < P.W) & (e < wv);
       vwork[j] = ((vt & ~31) + j * W2_V) < wv;     // warp-uniform: this block of 32 columns is scanned
     }
-    int U[COLS][NS * 4 * MAXK];
+    int U[TM ? 1 : COLS][TM ? 1 : NS * 4 * MAXK];
+    // TM: this thread's TMEM lane (its warp's lane quarter) and 4 MAXK columns (three V warps share
+    // a quarter)
+    const unsigned taddr = TM ? tmem_slot + ((unsigned)(32 * ((tid >> 5) & 3)) << 16) +
+                                    (unsigned)(((tid - V0) >> 7) * BF_X_TMSTRIDE)
+                              : 0u;
     // prefetched taps: COLS == 1 the next row's; COLS == 2 the next (row, column) in the order
     // (y, 0), (y, 1), (y + 1, 0), ... (one column's worth of registers)
     float Ipre[NB][2];
 #pragma unroll
     for (int j = 0; j < COLS; ++j)
-      if (vwork[j] && !BF_X_NOV) v_init<MAXK, NB, NS, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, U[j]);
+      if (vwork[j] && !BF_X_NOV) {
+        if constexpr (TM) tm::v_init<MAXK, NB, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, taddr);
+        else v_init<MAXK, NB, NS, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, U[j]);
+      }
     load_taps<NB, U8>(P, in, fbase, col[0], colok[0], y0, Ipre);
     for (int y = y0; y < yend; ++y) {
       const int b = (y - y0) & 1;
@@ -185,7 +255,8 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
             Icur[bb][1] = Ipre[bb][1];
           }
           if (y + 1 < yend) load_taps<NB, U8>(P, in, fbase, col[0], colok[0], y + 1, Ipre);
-          v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP, GroupSync, CL>(P, lut, colok[0], y, t0, nkc, Icur, U[0], Ub, &hook);
+          if constexpr (TM) tm::v_row<MAXK, NB, U8, CONSEC, FULL, UP, CL>(P, lut, colok[0], y, t0, nkc, Icur, taddr, Ub, hook);
+          else v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP, GroupSync, CL>(P, lut, colok[0], y, t0, nkc, Icur, U[0], Ub, &hook);
         } else {
           for (int g = 0; g < ngrp; ++g) {
             hook.begin(g);
@@ -224,7 +295,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       for (int g = 0; g < ngrp; ++g) bar_sync(BAR_U_EMPTY + 2 * ((y - y0) & 1) + g, n_uempty);
   } else if (tid >= S0) {
     // ------------------------------------------------------------ S role: prefix scans
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(OREG));
+    if constexpr (OREG < LREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(OREG));
     const int g = (tid - S0) >> 5;
     if (g < ngrp) {
       const int slot = 32 * g + (tid & 31);
@@ -238,8 +309,10 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ FH role
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(OREG));
-    const int o = tid - H0;
+    if constexpr (FHREG > LREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(FHREG));
+    else if constexpr (FHREG < LREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(FHREG));
+    const bool fhb = SPLIT && tid >= W2_SPLIT_FH;  // SPLIT: FH-B (terms 8 .. nk-1) of pixel o
+    const int o = SPLIT ? (tid & (W2_SPLIT_FH - 1)) : tid - H0;
     const bool act = o < TWv;
     const bool wact = (o & ~31) < TWv;             // warp has pixels of the strip
     const int oc = act ? o : 0;
@@ -274,6 +347,15 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < MAXK; ++i) {
           if (FULL || i < nkc) {
+            if (SPLIT && (i >> 3) != (fhb ? 1 : 0)) {
+              // another thread's group: FH-B still runs group 0's recurrence steps (no weights), the
+              // same sequence the one-thread combine runs, so its weights are bitwise the same
+              if (fhb && i > 0 && !BF_X_NOW) {
+                gk.step();
+                if (!CONSEC) extra_steps(P.kstep[t0 + i], [&] { gk.step(); });
+              }
+              continue;
+            }
             if ((i & 7) == 0) bar_sync(BAR_Q_FULL + 2 * b + (i >> 3), n_qfull);
             if (!DUMP && i > 0 && !BF_X_NOW) {   // k_i - k_{i-1} >= 1 steps
               gk.step();
@@ -345,12 +427,34 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
           }
         }
       } else {   // warp wholly past the strip: only the barriers
-        for (int g = 0; g < ngrp; ++g) {
+        const int g0 = (SPLIT && fhb) ? 1 : 0, g1 = SPLIT ? g0 + 1 : ngrp;
+        for (int g = g0; g < g1; ++g) {
           bar_sync(BAR_Q_FULL + 2 * b + g, n_qfull);
           bar_arrive(BAR_U_EMPTY + 2 * b + g, n_uempty);
         }
       }
       if constexpr (DUMP) continue;
+      if constexpr (SPLIT) {   // FH-B's partial sums to FH-A through the slot of this row parity
+        longlong2* part = red + 2 * (b * W2_SPLIT_FH + o);
+        if (fhb) {
+          if (y - y0 >= 2) bar_sync(BAR_P_EMPTY + b, n_part);   // FH-A has read row y - 2's slot
+          if (act) {
+            part[0] = make_longlong2(num[0], den[0]);
+            part[1] = make_longlong2(num[1], den[1]);
+          }
+          bar_arrive(BAR_P_FULL + b, n_part);
+          continue;
+        }
+        bar_sync(BAR_P_FULL + b, n_part);
+        if (act) {   // exact integer sums: the result is that of one thread doing every term
+          const longlong2 v0 = part[0], v1 = part[1];
+          num[0] += v0.x;
+          den[0] += v0.y;
+          num[1] += v1.x;
+          den[1] += v1.y;
+        }
+        bar_arrive(BAR_P_EMPTY + b, n_part);
+      }
       if constexpr (CL) {
         const unsigned ph = ((y - y0) >> 1) & 1;
         if (rank > 0) {
@@ -399,10 +503,20 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       }
     }
   }
+  if constexpr (SPLIT) {   // FH-B: FH-A's last two slot releases
+    if (tid >= W2_SPLIT_FH && tid < 2 * W2_SPLIT_FH)
+      for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_P_EMPTY + ((y - y0) & 1), n_part);
+  }
   if constexpr (CL) {
     // no CTA may leave while its shared memory can still be the target of a remote operation
     __syncwarp();
     cluster_sync();
+  }
+  if constexpr (TM) {   // every V warp's last TMEM access is done: the allocating warp frees
+    tm::fence_before();
+    __syncthreads();
+    tm::fence_after();
+    if (!BF_X_TMNODEALLOC && tid >= BF_X_TMWARP * 32 && tid < BF_X_TMWARP * 32 + 32) tm::dealloc(tmem_slot, TM_COLS);
   }
 }
 
@@ -414,7 +528,7 @@ cudaError_t go(const KParams& P, const void* in, float* out, longlong2* ws, dim3
   if constexpr (CL) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(W2_THREADS);
+    cfg.blockDim = dim3(w2_threads<MAXK, COLS, NPL, CL, DUMP>());
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -427,7 +541,7 @@ cudaError_t go(const KParams& P, const void* in, float* out, longlong2* ws, dim3
     e = cudaLaunchKernelEx(&cfg, kfn, P, in, out, ws);
     if (e != cudaSuccess) return e;
   } else {
-    kfn<<<grid, W2_THREADS, smem, st>>>(P, in, out, ws);
+    kfn<<<grid, w2_threads<MAXK, COLS, NPL, CL, DUMP>(), smem, st>>>(P, in, out, ws);
   }
   return cudaGetLastError();
 }

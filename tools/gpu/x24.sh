@@ -1,0 +1,2 @@
+rm -f gpurun_out/x24.txt
+for l in tmv80 tmv88; do echo "== $l" >> gpurun_out/x24.txt; CUDA_LAUNCH_BLOCKING=1 timeout 200 python tools/time_libs.py cfg0,cfg2 tools/var/libbf_$l.so >> gpurun_out/x24.txt 2>&1; done
