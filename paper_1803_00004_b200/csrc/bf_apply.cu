@@ -390,20 +390,13 @@ size_t smem_ws(const KParams& P, int MAXK, int nk, bool u8, int& f_off, int& l_o
 }
 
 // kernel 2b: mbarriers, two U' row buffers of the CTA's channels, LUTs (u8), cluster reduction rows
-size_t smem_ws2(int cols, int nkc, int tw, int G, bool u8, bool split, int& l_off, int& r_off) {
+size_t smem_ws2(int cols, int nkc, int tw, int G, bool u8, int& l_off, int& r_off) {
   size_t off = 64 + (sizeof(int) * 2 * 4 * (size_t)nkc * w2_up(cols) + 15) / 16 * 16;
   l_off = (int)off;
   if (u8) off += 256 * (sizeof(float2) + sizeof(double2));
   r_off = (int)off;
   if (G > 1) off += 2 * (size_t)tw * 2 * sizeof(longlong2);   // per row parity: sum of the senders' (num_b, den_b)
-  if (split) off += 2 * (size_t)W2_SPLIT_FH * 2 * sizeof(longlong2);   // per row parity: FH-B's (num_b, den_b)
   return off;
-}
-
-// kernel 2b with two FH threads per pixel (bf_ws2.cuh w2_split): 16 terms per CTA, one range plan,
-// no cluster, no channel dump
-bool ws2_split(int cols, int tpc, int G, bool multi, bool dump) {
-  return BF_SPLIT && cols == 1 && tpc == 16 && G == 1 && !multi && !dump;
 }
 
 struct Req {
@@ -485,8 +478,7 @@ bf_status prepare(const Req& R, const bf_plan* p, Launch& L) {
       const int G = (nterm + tpc - 1) / tpc;
       if (G > 4 || (multi && G > 1) || (R.dump && G > 1)) continue;
       const int nkc = std::min(tpc, nterm);
-      const bool split = ws2_split(cols, tpc, G, multi, R.dump);
-      const int twmax = std::min(split ? W2_SPLIT_FH : w2_nfh(cols), W2_V * cols - halo);
+      const int twmax = std::min(w2_nfh(cols), W2_V * cols - halo);
       LaunchSpec s{};
       s.kern = KERN_WS2;
       s.COLS = cols;
@@ -496,7 +488,7 @@ bf_status prepare(const Req& R, const bf_plan* p, Launch& L) {
       for (int tw = twmax; tw >= 1; tw = (tw % 32) ? tw - tw % 32 : tw - 32) {
         if (tw != twmax && tw < 128) break;
         int lo, ro;
-        const size_t smem = smem_ws2(cols, nkc, tw, G, u8, split, lo, ro);
+        const size_t smem = smem_ws2(cols, nkc, tw, G, u8, lo, ro);
         if (smem > 227 * 1024) continue;
         const int wv = (tw + halo + 7) & ~7;
         // row time: warp-instructions per role (ncu, cfg2, 64 channels: V 694 per 32 extended
@@ -542,7 +534,7 @@ bf_status prepare(const Req& R, const bf_plan* p, Launch& L) {
       if (multi) L.spec.FULL = false;
       L.passes = R.dump ? (nk + 15) / 16 : 1;
       L.name = "bf_ws2_kernel";
-      L.threads = ws2_split(L.spec.COLS, P.tpc, P.G, multi, R.dump) ? W2_SPLIT_THREADS : W2_THREADS;
+      L.threads = W2_THREADS;
       if (R.band_rows > 0) P.TH = std::max(1, std::min(Hr, R.band_rows));
       const int nb = (Hr + P.TH - 1) / P.TH;
       L.grid = dim3((unsigned)(((W + P.TW - 1) / P.TW) * P.G), (unsigned)nb, (unsigned)R.n_frames);

@@ -96,13 +96,6 @@ constexpr int WS_V = 256, WS_S = 64, WS_F = 192, WS_C = 128, WS_THREADS = WS_V +
 constexpr int WS_H = WS_S + WS_F;
 // kernel 2b (bf_ws2_kernel): V threads (extended columns / COLS), S threads, FH threads (outputs)
 constexpr int W2_V = 384, W2_THREADS = 768;
-// kernel 2b with two FH threads per pixel (see bf_ws2.cuh, SPLIT): 2 x 256 FH + 64 S + 384 V
-// SPLIT is measured slower than one FH thread per pixel (cfg2 1.97 vs 1.90 ms, cfg1 0.173 vs
-// 0.145 ms: DESIGN.md 8) and off by default; -DBF_SPLIT=1 builds it (host and kernels alike)
-#ifndef BF_SPLIT
-#define BF_SPLIT 0
-#endif
-constexpr int W2_SPLIT_FH = 256, W2_SPLIT_THREADS = 2 * W2_SPLIT_FH + 64 + W2_V, W2_SPLIT_LAUNCH_REG = 64;
 constexpr int w2_nfh(int cols) { return cols == 1 ? 320 : 352; }
 constexpr int w2_ns(int cols) { return cols == 1 ? 64 : 32; }
 constexpr int w2_up(int cols) { return W2_V * cols + 4; }   // == 4 mod 32: conflict-free 16-byte accesses

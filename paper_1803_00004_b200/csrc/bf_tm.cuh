@@ -10,12 +10,6 @@
 
 #include "bf_device.cuh"
 
-#ifndef BF_X_TMINIT0
-#define BF_X_TMINIT0 0
-#endif
-#ifndef BF_X_TMROW0
-#define BF_X_TMROW0 0
-#endif
 namespace bf {
 namespace tm {
 
@@ -67,7 +61,7 @@ __device__ __forceinline__ void v_init(const KParams& P, const void* __restrict_
     int ub[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) ub[c] = P.urnd;
-    for (int v = P.vmin; v <= (BF_X_TMINIT0 ? P.vmin - 1 : P.vmax); v += 2) {
+    for (int v = P.vmin; v <= P.vmax; v += 2) {
       const int ra = y0 - 1 + v, rb = ra + 1;
       const bool oka = colok && ra >= 0 && ra < P.H;
       const bool okb = colok && v + 1 <= P.vmax && rb >= 0 && rb < P.H;
@@ -155,7 +149,7 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
   for (int i = 0; i < MAXK; ++i) {
     if (FULL || i < nk) {
       if ((i & 7) == 0) hook.begin(i >> 3);
-      if ((i & 3) == 0 && !BF_X_TMROW0) {
+      if ((i & 3) == 0) {
         ld16(taddr + 4 * i, ub);
         wait_ld();
       }
@@ -179,7 +173,7 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c) Ucol[(4 * i + c) * UP] = ub[4 * j + c] >> P.ush;
-      if ((j == 3 || (FULL ? i + 1 == MAXK : i + 1 == nk)) && !BF_X_TMROW0) st16(taddr + 4 * (i - j), ub);
+      if (j == 3 || (FULL ? i + 1 == MAXK : i + 1 == nk)) st16(taddr + 4 * (i - j), ub);
       if ((i & 7) == 7 || (FULL ? i + 1 == MAXK : i + 1 == nk)) hook.end(i >> 3);
     }
   }

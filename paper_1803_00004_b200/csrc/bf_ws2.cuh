@@ -88,27 +88,12 @@ constexpr int MBAR_BYTES = 64;
 #ifndef BF_TM_VREG
 #define BF_TM_VREG 72
 #endif
-#ifndef BF_X_TMSTRIDE
-#define BF_X_TMSTRIDE (4 * MAXK)
-#endif
 #ifndef BF_TM_FHREG
 #define BF_TM_FHREG 80
 #endif
 constexpr int W2_LAUNCH_REG = 80;   // registers per thread at launch (768 threads, one CTA per SM)
-#ifndef BF_SPLIT_VREG
-#define BF_SPLIT_VREG 80
-#endif
-constexpr int BAR_P_FULL = 12, BAR_P_EMPTY = 14;   // SPLIT: FH-B -> FH-A partial-sum slots (per row parity)
-#ifndef BF_X_TMWARP
-#define BF_X_TMWARP (V0 / 32)
-#endif
-#ifndef BF_X_TMNODEALLOC
-#define BF_X_TMNODEALLOC 0
-#endif
-#ifndef BF_X_TMCOLS
-#define BF_X_TMCOLS 256
-#endif
-constexpr unsigned TM_COLS = BF_X_TMCOLS;   // TMEM columns: 3 V warps per lane quarter x 64 (4 MAXK, MAXK <= 16)
+constexpr int BAR_TM_DONE = 15;   // V warps: every TMEM access done (the allocating warp then frees)
+constexpr unsigned TM_COLS = 256;   // TMEM columns: 3 V warps per lane quarter x 64 (4 MAXK, MAXK <= 16)
 
 // diagnostic builds only (tools/build_variant.py): drop one role's arithmetic, keep its barriers
 #ifndef BF_X_NOV
@@ -127,45 +112,29 @@ constexpr unsigned TM_COLS = BF_X_TMCOLS;   // TMEM columns: 3 V warps per lane 
 #define BF_X_NOLDS 0
 #endif   // mbarriers at the start of shared memory (FULL[2], EMPTY[2])
 
-// SPLIT: two FH threads per output pixel, one per 32-channel group (terms 0-7 and 8-15), twice the
-// FH warps for the latency-bound combine; FH-B hands its partial sums to FH-A through shared memory.
-// Needs the V state in TMEM (registers) and one range plan without a cluster.
-template <int MAXK, int COLS, int NPL, bool CL, bool DUMP>
-constexpr bool w2_split() {
-  return COLS == 1 && MAXK == 16 && BF_TM && NPL == 1 && !CL && !DUMP && BF_SPLIT;
-}
-template <int MAXK, int COLS, int NPL, bool CL, bool DUMP>
-constexpr int w2_threads() {
-  return w2_split<MAXK, COLS, NPL, CL, DUMP>() ? W2_SPLIT_THREADS : W2_THREADS;
-}
-
 template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL, int NPL, int COLS, bool CL, bool DUMP>
-__global__ void __launch_bounds__(w2_threads<MAXK, COLS, NPL, CL, DUMP>(), 1)
+__global__ void __launch_bounds__(W2_THREADS, 1)
     bf_ws2_kernel(const KParams P, const void* __restrict__ in, float* __restrict__ out, longlong2* __restrict__ ws) {
   constexpr int NS = Form<FORM>::NS, NB = Form<FORM>::NBY, NBX = Form<FORM>::NBX;
   constexpr int M = NS * NBX;
   static_assert(NS == 1 && M <= 2, "the FH role handles separable forms with at most two x boxes");
   static_assert(COLS == 1 || MAXK == 8, "two columns per V thread: 8 terms per CTA (one channel group)");
-  constexpr bool SPLIT = w2_split<MAXK, COLS, NPL, CL, DUMP>();
-  constexpr int NTH = w2_threads<MAXK, COLS, NPL, CL, DUMP>();
-  constexpr int NFH = SPLIT ? 2 * W2_SPLIT_FH : w2_nfh(COLS), NSW = w2_ns(COLS);
-  constexpr int NFG = SPLIT ? W2_SPLIT_FH : NFH;   // FH threads per channel group
+  constexpr int NTH = W2_THREADS;
+  constexpr int NFH = w2_nfh(COLS), NSW = w2_ns(COLS);
   constexpr int H0 = 0, S0 = NFH, V0 = NFH + NSW;
   static_assert(V0 + W2_V == NTH, "role sizes");
-  constexpr int LREG = SPLIT ? W2_SPLIT_LAUNCH_REG : W2_LAUNCH_REG;
+  constexpr int LREG = W2_LAUNCH_REG;
   constexpr int UP = w2_up(COLS);
   constexpr bool PB = NPL == 1 && !DUMP;   // per-box accumulators (see the FH role)
   // TM: the V role's sliding sums in tensor memory (bf_tm.cuh; one column per V thread), which
   // moves registers from V to the latency-bound FH role
-  // (MAXK == 8 instantiations trap in the TMEM path on sm_100a: under investigation, registers there)
-  constexpr bool TM = COLS == 1 && MAXK == 16 && BF_TM;
+  constexpr bool TM = COLS == 1 && BF_TM;
   // registers per role (setmaxnreg; the pool is the launch's LREG x NTH):
-  //   SPLIT  V 384 x 80 + FH 512 x 48 + S 64 x 48 = 58368 <= 960 x 64
   //   TM     V 384 x 72 + FH 320 x 80 + S 64 x 48 = 56320 <= 768 x 80
   //   else   V 384 x 112 + (FH + S) 384 x 48      = 61440
-  constexpr int VREG = SPLIT ? BF_SPLIT_VREG : (TM ? BF_TM_VREG : (NPL > 1 ? 104 : 112));
+  constexpr int VREG = TM ? BF_TM_VREG : (NPL > 1 ? 104 : 112);
   constexpr int OREG = NPL > 1 ? 56 : 48;
-  constexpr int FHREG = SPLIT ? 48 : (TM ? BF_TM_FHREG : OREG);
+  constexpr int FHREG = TM ? BF_TM_FHREG : OREG;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem_raw);   // FULL[2], EMPTY[2]
   int* Ubuf = reinterpret_cast<int*>(smem_raw + MBAR_BYTES);                     // [2][4 nk][UP]
@@ -187,14 +156,13 @@ __global__ void __launch_bounds__(w2_threads<MAXK, COLS, NPL, CL, DUMP>(), 1)
   const int wv = P.wv;                            // extended columns scanned (multiple of 8, <= W2_V * COLS)
   const int srow = 4 * nkc * UP;                  // ints per U' buffer
   constexpr int n_ufull = W2_V + 32;              // U_FULL: V arrive, S_g sync
-  constexpr int n_uempty = W2_V + NFG;            // U_EMPTY: FH (of the group) arrive, V sync
-  constexpr int n_qfull = 32 + NFG;               // Q_FULL: S_g arrive, FH sync
-  constexpr int n_part = 2 * W2_SPLIT_FH;         // P_FULL / P_EMPTY (SPLIT): FH-A and FH-B
+  constexpr int n_uempty = W2_V + NFH;            // U_EMPTY: FH arrive, V sync
+  constexpr int n_qfull = 32 + NFH;               // Q_FULL: S_g arrive, FH sync
 
   fill_luts<U8>(P, lut, lut64, tid, NTH);
   __shared__ unsigned tmem_slot;
   if constexpr (TM) {
-    if (tid >= BF_X_TMWARP * 32 && tid < BF_X_TMWARP * 32 + 32) tm::alloc(&tmem_slot, TM_COLS);   // one warp allocates
+    if (tid >= V0 && tid < V0 + 32) tm::alloc(&tmem_slot, TM_COLS);   // the first V warp allocates
     tm::fence_before();
   }
   if constexpr (CL) {
@@ -230,7 +198,7 @@ __global__ void __launch_bounds__(w2_threads<MAXK, COLS, NPL, CL, DUMP>(), 1)
     // TM: this thread's TMEM lane (its warp's lane quarter) and 4 MAXK columns (three V warps share
     // a quarter)
     const unsigned taddr = TM ? tmem_slot + ((unsigned)(32 * ((tid >> 5) & 3)) << 16) +
-                                    (unsigned)(((tid - V0) >> 7) * BF_X_TMSTRIDE)
+                                    (unsigned)(((tid - V0) >> 7) * 4 * MAXK)
                               : 0u;
     // prefetched taps: COLS == 1 the next row's; COLS == 2 the next (row, column) in the order
     // (y, 0), (y, 1), (y + 1, 0), ... (one column's worth of registers)
@@ -293,6 +261,12 @@ __global__ void __launch_bounds__(w2_threads<MAXK, COLS, NPL, CL, DUMP>(), 1)
     // drain: the FH warps' last releases
     for (int y = max(y0, yend - 2); y < yend; ++y)
       for (int g = 0; g < ngrp; ++g) bar_sync(BAR_U_EMPTY + 2 * ((y - y0) & 1) + g, n_uempty);
+    if constexpr (TM) {   // every V warp's TMEM accesses are done: the allocating (V) warp frees
+      tm::fence_before();
+      bar_sync(BAR_TM_DONE, W2_V);
+      tm::fence_after();
+      if (tid < V0 + 32) tm::dealloc(tmem_slot, TM_COLS);
+    }
   } else if (tid >= S0) {
     // ------------------------------------------------------------ S role: prefix scans
     if constexpr (OREG < LREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(OREG));
@@ -311,8 +285,7 @@ __global__ void __launch_bounds__(w2_threads<MAXK, COLS, NPL, CL, DUMP>(), 1)
     // ------------------------------------------------------------ FH role
     if constexpr (FHREG > LREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(FHREG));
     else if constexpr (FHREG < LREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(FHREG));
-    const bool fhb = SPLIT && tid >= W2_SPLIT_FH;  // SPLIT: FH-B (terms 8 .. nk-1) of pixel o
-    const int o = SPLIT ? (tid & (W2_SPLIT_FH - 1)) : tid - H0;
+    const int o = tid - H0;
     const bool act = o < TWv;
     const bool wact = (o & ~31) < TWv;             // warp has pixels of the strip
     const int oc = act ? o : 0;
@@ -347,15 +320,6 @@ __global__ void __launch_bounds__(w2_threads<MAXK, COLS, NPL, CL, DUMP>(), 1)
 #pragma unroll
         for (int i = 0; i < MAXK; ++i) {
           if (FULL || i < nkc) {
-            if (SPLIT && (i >> 3) != (fhb ? 1 : 0)) {
-              // another thread's group: FH-B still runs group 0's recurrence steps (no weights), the
-              // same sequence the one-thread combine runs, so its weights are bitwise the same
-              if (fhb && i > 0 && !BF_X_NOW) {
-                gk.step();
-                if (!CONSEC) extra_steps(P.kstep[t0 + i], [&] { gk.step(); });
-              }
-              continue;
-            }
             if ((i & 7) == 0) bar_sync(BAR_Q_FULL + 2 * b + (i >> 3), n_qfull);
             if (!DUMP && i > 0 && !BF_X_NOW) {   // k_i - k_{i-1} >= 1 steps
               gk.step();
@@ -427,34 +391,12 @@ __global__ void __launch_bounds__(w2_threads<MAXK, COLS, NPL, CL, DUMP>(), 1)
           }
         }
       } else {   // warp wholly past the strip: only the barriers
-        const int g0 = (SPLIT && fhb) ? 1 : 0, g1 = SPLIT ? g0 + 1 : ngrp;
-        for (int g = g0; g < g1; ++g) {
+        for (int g = 0; g < ngrp; ++g) {
           bar_sync(BAR_Q_FULL + 2 * b + g, n_qfull);
           bar_arrive(BAR_U_EMPTY + 2 * b + g, n_uempty);
         }
       }
       if constexpr (DUMP) continue;
-      if constexpr (SPLIT) {   // FH-B's partial sums to FH-A through the slot of this row parity
-        longlong2* part = red + 2 * (b * W2_SPLIT_FH + o);
-        if (fhb) {
-          if (y - y0 >= 2) bar_sync(BAR_P_EMPTY + b, n_part);   // FH-A has read row y - 2's slot
-          if (act) {
-            part[0] = make_longlong2(num[0], den[0]);
-            part[1] = make_longlong2(num[1], den[1]);
-          }
-          bar_arrive(BAR_P_FULL + b, n_part);
-          continue;
-        }
-        bar_sync(BAR_P_FULL + b, n_part);
-        if (act) {   // exact integer sums: the result is that of one thread doing every term
-          const longlong2 v0 = part[0], v1 = part[1];
-          num[0] += v0.x;
-          den[0] += v0.y;
-          num[1] += v1.x;
-          den[1] += v1.y;
-        }
-        bar_arrive(BAR_P_EMPTY + b, n_part);
-      }
       if constexpr (CL) {
         const unsigned ph = ((y - y0) >> 1) & 1;
         if (rank > 0) {
@@ -503,20 +445,10 @@ __global__ void __launch_bounds__(w2_threads<MAXK, COLS, NPL, CL, DUMP>(), 1)
       }
     }
   }
-  if constexpr (SPLIT) {   // FH-B: FH-A's last two slot releases
-    if (tid >= W2_SPLIT_FH && tid < 2 * W2_SPLIT_FH)
-      for (int y = max(y0, yend - 2); y < yend; ++y) bar_sync(BAR_P_EMPTY + ((y - y0) & 1), n_part);
-  }
   if constexpr (CL) {
     // no CTA may leave while its shared memory can still be the target of a remote operation
     __syncwarp();
     cluster_sync();
-  }
-  if constexpr (TM) {   // every V warp's last TMEM access is done: the allocating warp frees
-    tm::fence_before();
-    __syncthreads();
-    tm::fence_after();
-    if (!BF_X_TMNODEALLOC && tid >= BF_X_TMWARP * 32 && tid < BF_X_TMWARP * 32 + 32) tm::dealloc(tmem_slot, TM_COLS);
   }
 }
 
@@ -528,7 +460,7 @@ cudaError_t go(const KParams& P, const void* in, float* out, longlong2* ws, dim3
   if constexpr (CL) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(w2_threads<MAXK, COLS, NPL, CL, DUMP>());
+    cfg.blockDim = dim3(W2_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -541,7 +473,7 @@ cudaError_t go(const KParams& P, const void* in, float* out, longlong2* ws, dim3
     e = cudaLaunchKernelEx(&cfg, kfn, P, in, out, ws);
     if (e != cudaSuccess) return e;
   } else {
-    kfn<<<grid, w2_threads<MAXK, COLS, NPL, CL, DUMP>(), smem, st>>>(P, in, out, ws);
+    kfn<<<grid, W2_THREADS, smem, st>>>(P, in, out, ws);
   }
   return cudaGetLastError();
 }
