@@ -116,7 +116,9 @@ __device__ __forceinline__ void v_init(const KParams& P, const void* __restrict_
 }
 
 // v_row (bf_device.cuh) with the state in TMEM, one batch of four terms in registers at a time.
-template <int MAXK, int NB, bool U8, bool CONSEC, bool FULL, int UP, bool POW>
+// HOOK: the per-group hand-off barriers run inside (one column per thread); without, the caller
+// brackets the columns of a thread (COLS = 2, one channel group).
+template <int MAXK, int NB, bool U8, bool CONSEC, bool FULL, int UP, bool POW, bool HOOK = true>
 __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool colok, int y, int t0, int nk,
                                       const float (&Ipre)[NB][2], unsigned taddr, int* Ucol, const GroupSync& hook) {
   u64 QS[NB], QI[NB];
@@ -148,7 +150,7 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
 #pragma unroll
   for (int i = 0; i < MAXK; ++i) {
     if (FULL || i < nk) {
-      if ((i & 7) == 0) hook.begin(i >> 3);
+      if (HOOK && (i & 7) == 0) hook.begin(i >> 3);
       if ((i & 3) == 0) {
         ld16(taddr + 4 * i, ub);
         wait_ld();
@@ -174,7 +176,7 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
 #pragma unroll
       for (int c = 0; c < 4; ++c) Ucol[(4 * i + c) * UP] = ub[4 * j + c] >> P.ush;
       if (j == 3 || (FULL ? i + 1 == MAXK : i + 1 == nk)) st16(taddr + 4 * (i - j), ub);
-      if ((i & 7) == 7 || (FULL ? i + 1 == MAXK : i + 1 == nk)) hook.end(i >> 3);
+      if (HOOK && ((i & 7) == 7 || (FULL ? i + 1 == MAXK : i + 1 == nk))) hook.end(i >> 3);
     }
   }
 }

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   constexpr bool PB = NPL == 1 && !DUMP;   // per-box accumulators (see the FH role)
   // TM: the V role's sliding sums in tensor memory (bf_tm.cuh; one column per V thread), which
   // moves registers from V to the latency-bound FH role
-  constexpr bool TM = COLS == 1 && BF_TM;
+  constexpr bool TM = BF_TM;
   // registers per role (setmaxnreg; the pool is the launch's LREG x NTH):
   //   TM     V 384 x 72 + FH 320 x 80 + S 64 x 48 = 56320 <= 768 x 80
   //   else   V 384 x 112 + (FH + S) 384 x 48      = 61440
@@ -195,10 +195,10 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       vwork[j] = ((vt & ~31) + j * W2_V) < wv;     // warp-uniform: this block of 32 columns is scanned
     }
     int U[TM ? 1 : COLS][TM ? 1 : NS * 4 * MAXK];
-    // TM: this thread's TMEM lane (its warp's lane quarter) and 4 MAXK columns (three V warps share
-    // a quarter)
+    // TM: this thread's TMEM lane (its warp's lane quarter) and COLS x 4 MAXK columns (three V warps
+    // share a quarter; column j of the thread at + 4 MAXK j)
     const unsigned taddr = TM ? tmem_slot + ((unsigned)(32 * ((tid >> 5) & 3)) << 16) +
-                                    (unsigned)(((tid - V0) >> 7) * 4 * MAXK)
+                                    (unsigned)(((tid - V0) >> 7) * COLS * 4 * MAXK)
                               : 0u;
     // prefetched taps: COLS == 1 the next row's; COLS == 2 the next (row, column) in the order
     // (y, 0), (y, 1), (y + 1, 0), ... (one column's worth of registers)
@@ -206,7 +206,9 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
 #pragma unroll
     for (int j = 0; j < COLS; ++j)
       if (vwork[j] && !BF_X_NOV) {
-        if constexpr (TM) tm::v_init<MAXK, NB, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, taddr);
+        if constexpr (TM)
+          tm::v_init<MAXK, NB, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc,
+                                                     taddr + 4 * MAXK * j);
         else v_init<MAXK, NB, NS, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, U[j]);
       }
     load_taps<NB, U8>(P, in, fbase, col[0], colok[0], y0, Ipre);
@@ -251,9 +253,14 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
             const int en = vt + jn * W2_V, cn = x0 - P.rlo_x + en;
             if (yn < yend) load_taps<NB, U8>(P, in, fbase, cn, (cn >= 0) & (cn < P.W) & (en < wv), yn, Ipre);
           }
-          if (((vt & ~31) + j * W2_V) < wv)
-            v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP, GroupSync, CL>(P, lut, okj, y, t0, nkc, Icur, U[j],
-                                                                    Ub + j * W2_V);
+          if (((vt & ~31) + j * W2_V) < wv) {
+            if constexpr (TM)
+              tm::v_row<MAXK, NB, U8, CONSEC, FULL, UP, CL, false>(P, lut, okj, y, t0, nkc, Icur, taddr + 4 * MAXK * j,
+                                                                   Ub + j * W2_V, hook);
+            else
+              v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP, GroupSync, CL>(P, lut, okj, y, t0, nkc, Icur, U[j],
+                                                                      Ub + j * W2_V);
+          }
         }
         hook.end(0);
       }
