@@ -86,7 +86,10 @@ constexpr int MBAR_BYTES = 64;
 #define BF_TM 1
 #endif
 #ifndef BF_TM_VREG
-#define BF_TM_VREG 72
+#define BF_TM_VREG 64
+#endif
+#ifndef BF_TM_VREG2
+#define BF_TM_VREG2 80
 #endif
 #ifndef BF_TM_FHREG
 #define BF_TM_FHREG 80
@@ -130,9 +133,11 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   // moves registers from V to the latency-bound FH role
   constexpr bool TM = BF_TM;
   // registers per role (setmaxnreg; the pool is the launch's LREG x NTH):
-  //   TM     V 384 x 72 + FH 320 x 80 + S 64 x 48 = 56320 <= 768 x 80
+  //   TM     V 384 x 64 + FH 320 x 80 + S 64 x 48 = 53248 <= 768 x 80 (measured: V at 64 is
+  //          1.83 ms on cfg2 against 1.89 at 72 and 80)
+  //          two columns: V 384 x 80 + FH 352 x 80 + S 32 x 48 = 60416 (cfg4 32.2 ms; 37.3 at 64)
   //   else   V 384 x 112 + (FH + S) 384 x 48      = 61440
-  constexpr int VREG = TM ? BF_TM_VREG : (NPL > 1 ? 104 : 112);
+  constexpr int VREG = TM ? (COLS == 2 ? BF_TM_VREG2 : BF_TM_VREG) : (NPL > 1 ? 104 : 112);
   constexpr int OREG = NPL > 1 ? 56 : 48;
   constexpr int FHREG = TM ? BF_TM_FHREG : OREG;
   extern __shared__ __align__(16) unsigned char smem_raw[];
