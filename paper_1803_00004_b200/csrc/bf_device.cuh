@@ -181,6 +181,22 @@ struct Rot2 {
   // (C, S) = (c1, s1)^k0 by binary powering (k0 < 64; k0 = 0 leaves (C, S) = (1, 0))
   __device__ __forceinline__ void start(int k0) {
     if (k0 == 0) return;
+    if ((k0 & (k0 - 1)) == 0) {
+      // k0 = 2^m (the cluster split's first terms, 8 and 16): the general loop below reduces to m
+      // squarings of (c1, s1) with the same operations; without its per-bit bookkeeping
+      u64 bc = C1, bs = S1;
+#pragma unroll 1
+      for (int k = k0; k > 1; k >>= 1) {
+        const u64 nbs = bs ^ 0x8000000080000000ull;
+        const u64 bcn = fma2(bs, nbs, mul2(bc, bc));
+        const u64 bsn = fma2(bc, bs, mul2(bs, bc));
+        bc = bcn;
+        bs = bsn;
+      }
+      C = bc;
+      S = bs;
+      return;
+    }
     u64 bc = C1, bs = S1, nbs = NS1;
     bool first = true;
 #pragma unroll 1

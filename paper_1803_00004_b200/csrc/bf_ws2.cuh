@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         pixel_angle<U8>(P, lut64, Ic, c1, s1);
         Cheb64 gk;
         gk.init(c1, s1);
+#pragma unroll 4
         for (int j = 0; j < k0; ++j) gk.step();
         const int* Qb = Ubuf + b * srow;
 #pragma unroll
