@@ -276,7 +276,7 @@ BF_API bf_status bf_apply_launches(const bf_plan* plan, int H, int W, int* n_lau
 /* Launch configuration bf_apply_batched(plan, ., ., n_frames, H, W, .) enqueues (bf_apply is
  * n_frames = 1): kernel name (a static string owned by the library), threads per CTA, grid
  * (strips x bands x frames), output tile (columns per strip, rows per band), dynamic shared
- * memory per CTA and the number of launches (passes). Pure host computation, no device work;
+ * memory per CTA, the number of launches (passes) and kernel 2b's warp-role map. Pure host computation, no device work;
  * the kernel choice and band height follow the same rules (bf_apply_args.kernel / band_rows)
  * as the apply call. Errors as bf_apply_launches. */
 typedef struct bf_launch_config {
@@ -290,6 +290,10 @@ typedef struct bf_launch_config {
   int terms_per_cta;             /* range terms one CTA evaluates per pass                   */
   int cols_per_thread;           /* extended columns per vertical-pass thread (kernel 2b)    */
   size_t workspace_bytes;        /* bf_workspace_size of the same call                       */
+  unsigned char warp_map[24];    /* kernel 2b: logical warp (role order: box-difference/combine
+                                  * warps, scan warps, vertical-pass warps) run by physical warp
+                                  * i; the working warps of each role are spread evenly over the
+                                  * four SM sub-partitions (i mod 4). All 0 for other kernels.  */
 } bf_launch_config;
 
 /* args may be NULL (as bf_apply); args->kernel / band_rows are honoured as in bf_apply_ex. */

@@ -39,7 +39,8 @@ class LaunchConfig(C.Structure):
     _fields_ = [("n_launches", C.c_int), ("kernel", C.c_char_p), ("threads_per_cta", C.c_int), ("grid_x", C.c_int),
                 ("grid_y", C.c_int), ("grid_z", C.c_int), ("tile_w", C.c_int), ("tile_h", C.c_int),
                 ("smem_bytes", C.c_size_t), ("cluster_size", C.c_int), ("terms_per_cta", C.c_int),
-                ("cols_per_thread", C.c_int), ("workspace_bytes", C.c_size_t)]
+                ("cols_per_thread", C.c_int), ("workspace_bytes", C.c_size_t),
+                ("warp_map", C.c_ubyte * 24)]
 
 
 class ApplyArgs(C.Structure):
@@ -303,7 +304,7 @@ def config(plan: Plan, H: int, W: int, n_frames: int = 1, args: ApplyArgs | None
     return {"kernel": c.kernel.decode(), "launches": c.n_launches, "threads_per_cta": c.threads_per_cta,
             "grid": (c.grid_x, c.grid_y, c.grid_z), "tile": (c.tile_w, c.tile_h), "smem_bytes": c.smem_bytes,
             "cluster": c.cluster_size, "terms_per_cta": c.terms_per_cta, "cols_per_thread": c.cols_per_thread,
-            "workspace_bytes": c.workspace_bytes}
+            "workspace_bytes": c.workspace_bytes, "warp_map": list(c.warp_map)}
 
 
 def shard_frames(n_frames: int, n_parts: int, part: int) -> tuple:

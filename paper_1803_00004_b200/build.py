@@ -20,7 +20,7 @@ LIB = os.path.join(HERE, "libbf.so")
 SOURCES = ["bf_plan.cpp", "bf_apply.cu", "bf_k_band.cu", "bf_k_ws.cu", "bf_k_ws2.cu", "bf_k_ws2m_u8.cu",
            "bf_k_ws2m_f32.cu", "bf_k_ws2c.cu", "bf_k_lit.cu", "bf_k_cache.cu",
            "bf_k_repair.cu"]
-HEADERS = ["bf_internal.h", "bf_params.h", "bf_device.cuh", "bf_walk.cuh", "bf_ws2.cuh"]
+HEADERS = ["bf_internal.h", "bf_params.h", "bf_device.cuh", "bf_walk.cuh", "bf_ws2.cuh", "bf_tm.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]
 

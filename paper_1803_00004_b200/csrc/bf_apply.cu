@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -358,6 +359,146 @@ bf_status repair_sink(const bf_apply_args& A, double wscale, double mfull, doubl
 }
 
 // The launches of one call: template choice, parameter block, grid, shared memory, passes.
+// Kernel 2b's warp roles (P.wmap, P.tmblk, P.tmcols). A warp runs on SM sub-partition (physical
+// warp id mod 4), and the roles' rows are joined by barriers, so the slowest sub-partition sets the
+// pace. The map places the WORKING warps of every role (the strip width leaves some FH / V warps
+// idle) by what a search over every count layout measured on the B200 (tools/wmap_search.py,
+// profiles/r2s5_wmap_search.txt; cfg2 1.85 -> 1.74 ms against consecutive warp ids):
+//   - the S warps share one sub-partition and that one stays light: the scans are the serial
+//     stretch between V and FH of every row, and a scan warp that has to share its issue port
+//     delays both;
+//   - FH and V warps are mixed on every sub-partition (a sub-partition of one role idles whenever
+//     that role waits at a barrier): the FH warps evenly over the other three, then the V warps
+//     one by one to the lightest. Loads: warp-instructions per row from ncu on cfg2 (FH 57 and
+//     V 41 per term, S 2 per column). The FH count next to the S warps is the one that leaves
+//     the largest load smallest;
+//   - inside a sub-partition the V warps take the lowest warp ids, then S, then FH.
+#ifndef BF_WMAP
+#define BF_WMAP 1
+#endif
+#ifndef BF_MINTH
+#define BF_MINTH 4   // least band height of kernel 2b (cfg0 at 16: 0.048 ms, at 4: 0.026 ms)
+#endif
+void ws2_warp_map(KParams& P, int cols, int maxk, int nkc) {
+  const int nfh = w2_nfh(cols) / 32, nsw = w2_ns(cols) / 32, nw = W2_THREADS / 32;
+  const int S0 = nfh, V0 = nfh + nsw;
+  double w[24];
+  for (int l = 0; l < nw; ++l) {
+    if (l < S0) w[l] = 32 * l < P.TW ? 57.0 * nkc : 0.0;
+    else if (l < V0) w[l] = (l - S0) < P.ngrp ? 2.0 * P.wv : 0.0;
+    else {
+      w[l] = 0.0;
+      for (int j = 0; j < cols; ++j)
+        if (32 * (l - V0) + j * W2_V < P.wv) w[l] += 41.0 * nkc;
+    }
+  }
+  int fa = 0, sa = 0;
+  for (int l = 0; l < S0; ++l) fa += w[l] > 0;
+  for (int l = S0; l < V0; ++l) sa += w[l] > 0;
+  const double wf = 57.0 * nkc, wsn = 2.0 * P.wv;
+  int vord[12], nva = 0;   // working V warps by descending load (two columns before one)
+  for (int l = V0; l < nw; ++l)
+    if (w[l] > 0) vord[nva++] = l;
+  std::stable_sort(vord, vord + nva, [&](int a, int b) { return w[a] > w[b]; });
+  const int cap = nw / 4;
+  int f_best[4] = {}, vsel_best[12] = {};
+  double best = -1.0, best_s = 0.0;
+  // sub-partition 0 runs the S warps; FH counts: f0 free, f1 >= f2 >= f3 (interchangeable)
+  // (at least one FH warp next to the S warps when there are four or more: measured better on
+  // every config than none)
+  for (int f0 = std::min(fa, cap - sa); BF_WMAP && f0 >= (fa >= 4 ? 1 : 0); --f0)
+    for (int f1 = std::min(fa - f0, cap); f1 >= 0; --f1)
+      for (int f2 = std::min(f1, fa - f0 - f1); f2 >= 0; --f2) {
+        const int f3 = fa - f0 - f1 - f2;
+        if (f3 < 0 || f3 > f2 || f1 - f3 > 1) continue;   // FH spread evenly over sub-partitions 1..3
+        const int f[4] = {f0, f1, f2, f3};
+        int n[4], vsel[12];
+        double ld[4];
+        for (int q = 0; q < 4; ++q) {
+          n[q] = f[q] + (q == 0 ? sa : 0);
+          ld[q] = f[q] * wf + (q == 0 ? sa * wsn : 0.0);
+        }
+        bool ok = true;
+        int nv[4] = {0, 0, 0, 0};
+        // V warps greedily to the lightest sub-partition with a free slot, evenly (counts differ by
+        // at most one: the band's initial state is computed per sub-partition by all its warps)
+        for (int i = 0; i < nva && ok; ++i) {
+          int bq = -1;
+          for (int q = 0; q < 4; ++q)
+            if (n[q] < cap && nv[q] < (nva + 3) / 4 && (bq < 0 || ld[q] < ld[bq] - 1e-9)) bq = q;
+          if (bq < 0) {
+            ok = false;
+            break;
+          }
+          vsel[i] = bq;
+          ++n[bq];
+          ++nv[bq];
+          ld[bq] += w[vord[i]];
+        }
+        for (int q = 0; q < 4; ++q) ok &= nv[q] >= nva / 4;
+        if (!ok) continue;
+        const double mx = std::max(std::max(ld[0], ld[1]), std::max(ld[2], ld[3]));
+        if (best < 0 || mx < best * (1.0 - 1e-9) || (mx < best * (1.0 + 1e-9) && ld[0] < best_s)) {
+          best = mx;
+          best_s = ld[0];
+          for (int q = 0; q < 4; ++q) f_best[q] = f[q];
+          for (int i = 0; i < nva; ++i) vsel_best[i] = vsel[i];
+        }
+      }
+  if (best < 0) {   // consecutive warp ids (BF_WMAP = 0, or nothing fits)
+    for (int l = 0; l < nw; ++l) P.wmap[l] = (unsigned char)l;
+  } else {
+    // physical layout: sub-partition q owns physical warps q, q + 4, ...: V, S, FH, idle
+    int slot[4] = {0, 0, 0, 0};
+    bool placed[24] = {};
+    auto put = [&](int l, int q) {
+      P.wmap[q + 4 * slot[q]++] = (unsigned char)l;
+      placed[l] = true;
+    };
+    for (int i = 0; i < nva; ++i) put(vord[i], vsel_best[i]);
+    for (int l = S0; l < V0; ++l)
+      if (w[l] > 0) put(l, 0);
+    int nf = 0;
+    for (int q = 0; q < 4; ++q)
+      for (int i = 0; i < f_best[q]; ++i) {
+        while (w[nf] <= 0) ++nf;
+        put(nf++, q);
+      }
+    for (int l = 0; l < nw; ++l)
+      if (!placed[l]) {
+        int q = 0;
+        while (slot[q] >= cap) ++q;
+        put(l, q);
+      }
+  }
+#ifdef BF_WMAP_ENV   // search builds only (tools/wmap_search.py): the map from the environment
+  if (const char* e = std::getenv("BF_WMAP_OVERRIDE")) {
+    int v[24], n = 0;
+    while (n < 24 && *e) {
+      v[n++] = (int)std::strtol(e, const_cast<char**>(&e), 10);
+      if (*e == ',') ++e;
+    }
+    if (n == nw)
+      for (int i = 0; i < nw; ++i) P.wmap[i] = (unsigned char)v[i];
+  }
+#endif
+  // TMEM blocks: the working V warps of a lane quarter in physical order (idle V warps never
+  // touch TMEM); the same lists deal the initial-state units to the quarter's warps
+  int vq[4] = {0, 0, 0, 0};
+  for (int pwi = 0; pwi < nw; ++pwi) {
+    const int l = P.wmap[pwi], q = pwi & 3;
+    P.tmblk[pwi] = 0;
+    if (l >= V0 && w[l] > 0) {
+      P.tmblk[pwi] = (unsigned char)vq[q];
+      P.vq[q][vq[q]++] = (unsigned char)(l - V0);
+    }
+  }
+  for (int q = 0; q < 4; ++q) P.nvq[q] = (unsigned char)vq[q];
+  const int need = std::max(std::max(vq[0], vq[1]), std::max(vq[2], vq[3])) * cols * 4 * maxk;
+  P.tmcols = 32;
+  while (P.tmcols < need) P.tmcols *= 2;
+}
+
 struct Launch {
   LaunchSpec spec;
   KParams P;
@@ -501,7 +642,7 @@ bf_status prepare(const Req& R, const bf_plan* p, Launch& L) {
         const int slots = G > 1 ? max_clusters(s, smem, G) : nsm;   // resident clusters (CTAs for G = 1)
         for (int nb = 1; nb <= Hr; ++nb) {
           const int TH = (Hr + nb - 1) / nb;
-          if (nb > 1 && TH < 16) break;
+          if (nb > 1 && TH < BF_MINTH) break;
           const long long units = strips * nb * R.n_frames;
           const long long waves = (units + slots - 1) / slots;
           const double cost = (double)waves * (TH * row + ry * init);
@@ -540,6 +681,7 @@ bf_status prepare(const Req& R, const bf_plan* p, Launch& L) {
       L.grid = dim3((unsigned)(((W + P.TW - 1) / P.TW) * P.G), (unsigned)nb, (unsigned)R.n_frames);
       P.nk = R.dump ? nkc0 : nk;
       P.ngrp = (4 * nkc0 + 31) / 32;
+      ws2_warp_map(P, L.spec.COLS, L.spec.MAXK, nkc0);
       return BF_OK;
     }
   }
@@ -809,6 +951,7 @@ bf_status run_general(const Req& R, const bf_plan* const* plans, int nplans, con
     *dry = bf_launch_config{total, L0.name, L0.threads, (int)L0.grid.x, (int)L0.grid.y, (int)L0.grid.z, L0.P.TW,
                             L0.P.TH, L0.smem, L0.P.G, L0.spec.kern == KERN_WS2 ? L0.P.tpc : L0.spec.MAXK,
                             L0.spec.COLS, wsb};
+    if (L0.spec.kern == KERN_WS2) std::memcpy(dry->warp_map, L0.P.wmap, sizeof(dry->warp_map));
     return BF_OK;
   }
   if (!A.d_workspace || A.workspace_bytes < wsb) return BF_ERR_WORKSPACE;
@@ -914,6 +1057,7 @@ bf_status run(const bf_plan* const* plans, int nplans, const void* d_in, float* 
     *dry = bf_launch_config{L.passes, L.name, L.threads, (int)L.grid.x, (int)L.grid.y, (int)L.grid.z, L.P.TW,
                             L.P.TH, L.smem, L.P.G, L.spec.kern == KERN_WS2 ? L.P.tpc : L.spec.MAXK, L.spec.COLS,
                             L.ws_bytes};
+    if (L.spec.kern == KERN_WS2) std::memcpy(dry->warp_map, L.P.wmap, sizeof(dry->warp_map));
     return BF_OK;
   }
   longlong2* ws = nullptr;

@@ -488,10 +488,11 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
 
 // Exclusive prefix of one U' row in place, 8 columns per step (two 16-byte loads / stores, one
 // IADD3 per column); int32 wrap-around keeps every box difference exact. Q[n] = total.
-__device__ __forceinline__ void prefix_row(int* Q, int n) {
-  int carry = 0;
+// prefix_part scans columns [e0, e1) with the running total carried in and returned (a row scanned
+// in pieces, as its columns become available, equals the row scanned at once).
+__device__ __forceinline__ int prefix_part(int* Q, int e0, int e1, int carry) {
 #pragma unroll 8
-  for (int e = 0; e < n; e += 8) {
+  for (int e = e0; e < e1; e += 8) {
     const int4 a = *reinterpret_cast<const int4*>(Q + e), b = *reinterpret_cast<const int4*>(Q + e + 4);
     const int o1 = carry + a.x;
     const int o2 = carry + a.x + a.y;
@@ -505,8 +506,9 @@ __device__ __forceinline__ void prefix_row(int* Q, int n) {
     *reinterpret_cast<int4*>(Q + e + 4) = make_int4(o4, o5, o6, o7);
     carry = o8;
   }
-  Q[n] = carry;
+  return carry;
 }
+__device__ __forceinline__ void prefix_row(int* Q, int n) { Q[n] = prefix_part(Q, 0, n, 0); }
 
 // Fallback bookkeeping (Q18): optional per-pixel mask and a warp-aggregated counter.
 __device__ __forceinline__ void note_fallback(unsigned long long* cnt, unsigned char* mask, long long pix, bool fb) {

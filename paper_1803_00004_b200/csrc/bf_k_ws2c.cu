@@ -11,6 +11,9 @@ cudaError_t by_flags(const LaunchSpec& s, const KParams& P, const void* in, floa
                      size_t smem, cudaStream_t st) {
   if (s.CONSEC && s.FULL) return ws2::go<MAXK, FORM, U8, true, true, 1, COLS, CL, false>(P, in, out, ws, grid, smem, st);
   if (s.CONSEC) return ws2::go<MAXK, FORM, U8, true, false, 1, COLS, CL, false>(P, in, out, ws, grid, smem, st);
+  // non-consecutive k with every CTA's term count known at compile time (cfg4: 24 Tukey terms = 3 x 8)
+  if constexpr (COLS == 2 && CL)
+    if (s.FULL) return ws2::go<MAXK, FORM, U8, false, true, 1, COLS, CL, false>(P, in, out, ws, grid, smem, st);
   return ws2::go<MAXK, FORM, U8, false, false, 1, COLS, CL, false>(P, in, out, ws, grid, smem, st);
 }
 

@@ -65,6 +65,11 @@ struct KParams {
   int wpar;                   // paired-load walker: parity of box 1's leave stream (0 / 1), -1 = scalar walker
   int wv;                     // kernel 2b: extended columns written and scanned (TW + halo rounded up to 8)
   int f_off, l_off, r_off;    // shared-memory carve-up: U' rows, F rows, LUTs, cluster reduction rows
+  unsigned char wmap[24];     // kernel 2b: physical warp -> logical warp (role and index; balanced over the SM sub-partitions)
+  unsigned char tmblk[24];    // kernel 2b: physical V warp -> its block of TMEM columns within its lane quarter
+  int tmcols;                 // kernel 2b: TMEM columns allocated (power of two >= 32)
+  unsigned char vq[4][6];     // kernel 2b: the working V warps (index in the V role) of lane quarter q, in TMEM block order
+  unsigned char nvq[4];       // kernel 2b: how many
   int G, tpc;                 // kernel 2b cluster split: G CTAs per cluster, CTA c owns terms [c tpc, c tpc + tpc)
   unsigned long long* fb_count;    // optional: += pixels that took the den <= 0 fallback (Q18)
   unsigned char* fb_mask;          // optional: 1 where the pixel took the fallback, else 0

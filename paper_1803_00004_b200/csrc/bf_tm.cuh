@@ -47,72 +47,71 @@ __device__ __forceinline__ void dealloc(unsigned taddr, unsigned cols) {
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// v_init (bf_device.cuh) with the state in TMEM: term batches outer (16 cells in registers), row
-// pairs inner; each batch re-derives its terms' channels from k0 with the same recurrence steps,
-// so every cell equals v_init's bitwise.
+// v_init (bf_device.cuh) with the state in TMEM, one batch of four terms (16 cells in registers)
+// of one column: row pairs inner; the batch re-derives its terms' channels from k0 with the same
+// recurrence steps, so every cell equals v_init's bitwise. Batches are independent, so any warp
+// of the column's lane quarter can compute any of them (the caller spreads them over every warp
+// of the SM sub-partition, the FH and S warps included: they have nothing else to do before the
+// first row). The caller waits for the stores (wait_st) and orders them before the first v_row.
 template <int MAXK, int NB, bool U8, bool CONSEC, bool FULL, bool POW>
-__device__ __forceinline__ void v_init(const KParams& P, const void* __restrict__ in, const float2* lut,
-                                       long long fbase, int col, bool colok, int y0, int t0, int nk, unsigned taddr) {
+__device__ __forceinline__ void v_init_batch(const KParams& P, const void* __restrict__ in, const float2* lut,
+                                             long long fbase, int col, bool colok, int y0, int t0, int nk, int bt,
+                                             unsigned taddr_bt) {
   const u64 MM = pk(MAGIC, MAGIC);
   const int k0 = P.kval[t0];
-#pragma unroll 1
-  for (int bt = 0; bt < MAXK / 4; ++bt) {
-    if (!FULL && 4 * bt >= nk) break;
-    int ub[16];
+  int ub[16];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) ub[c] = P.urnd;
-    for (int v = P.vmin; v <= P.vmax; v += 2) {
-      const int ra = y0 - 1 + v, rb = ra + 1;
-      const bool oka = colok && ra >= 0 && ra < P.H;
-      const bool okb = colok && v + 1 <= P.vmax && rb >= 0 && rb < P.H;
-      const float Ia = oka ? load_pixel(in, U8, fbase + (long long)ra * P.W + col) : 0.f;
-      const float Ib = okb ? load_pixel(in, U8, fbase + (long long)rb * P.W + col) : 0.f;
-      Rot2 g2;
-      if (U8) {
-        const float2 ta = lut[(int)Ia], tb = lut[(int)Ib];
-        g2.init(ta.x, ta.y, tb.x, tb.y);
-      } else {
-        u64 c1, s1;
-        base_angle_f32x2(Ia, Ib, P, c1, s1);
-        g2.init2(c1, s1);
-      }
-      u64 QS[NB], QI[NB];
+  for (int c = 0; c < 16; ++c) ub[c] = P.urnd;
+  for (int v = P.vmin; v <= P.vmax; v += 2) {
+    const int ra = y0 - 1 + v, rb = ra + 1;
+    const bool oka = colok && ra >= 0 && ra < P.H;
+    const bool okb = colok && v + 1 <= P.vmax && rb >= 0 && rb < P.H;
+    const float Ia = oka ? load_pixel(in, U8, fbase + (long long)ra * P.W + col) : 0.f;
+    const float Ib = okb ? load_pixel(in, U8, fbase + (long long)rb * P.W + col) : 0.f;
+    Rot2 g2;
+    if (U8) {
+      const float2 ta = lut[(int)Ia], tb = lut[(int)Ib];
+      g2.init(ta.x, ta.y, tb.x, tb.y);
+    } else {
+      u64 c1, s1;
+      base_angle_f32x2(Ia, Ib, P, c1, s1);
+      g2.init2(c1, s1);
+    }
+    u64 QS[NB], QI[NB];
 #pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const bool ina = oka && (b < P.nby) && v >= P.vlo[b] && v <= P.vhi[b];
-        const bool inb = okb && (b < P.nby) && v + 1 >= P.vlo[b] && v + 1 <= P.vhi[b];
-        QS[b] = pk(ina ? P.qs[0][b] : 0.f, inb ? P.qs[0][b] : 0.f);
-        QI[b] = pk(ina ? P.qsD[0][b] * Ia : 0.f, inb ? P.qsD[0][b] * Ib : 0.f);
-      }
-      if (POW) g2.start(k0);
-      else
-        for (int j = 0; j < k0; ++j) g2.step();
-      // the terms before this batch: recurrence steps only
-      for (int i = 1; i <= 4 * bt; ++i) {
-        g2.step();
-        if (!CONSEC) extra_steps(P.kstep[t0 + i], [&] { g2.step(); });
-      }
+    for (int b = 0; b < NB; ++b) {
+      const bool ina = oka && (b < P.nby) && v >= P.vlo[b] && v <= P.vhi[b];
+      const bool inb = okb && (b < P.nby) && v + 1 >= P.vlo[b] && v + 1 <= P.vhi[b];
+      QS[b] = pk(ina ? P.qs[0][b] : 0.f, inb ? P.qs[0][b] : 0.f);
+      QI[b] = pk(ina ? P.qsD[0][b] * Ia : 0.f, inb ? P.qsD[0][b] * Ib : 0.f);
+    }
+    if (POW) g2.start(k0);
+    else
+      for (int j = 0; j < k0; ++j) g2.step();
+    // the terms before this batch: recurrence steps only
+    for (int i = 1; i <= 4 * bt; ++i) {
+      g2.step();
+      if (!CONSEC) extra_steps(P.kstep[t0 + i], [&] { g2.step(); });
+    }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i = 4 * bt + j;
-        if (FULL || i < nk) {
-          if (j > 0) {
-            g2.step();
-            if (!CONSEC) extra_steps(P.kstep[t0 + i], [&] { g2.step(); });
-          }
+    for (int j = 0; j < 4; ++j) {
+      const int i = 4 * bt + j;
+      if (FULL || i < nk) {
+        if (j > 0) {
+          g2.step();
+          if (!CONSEC) extra_steps(P.kstep[t0 + i], [&] { g2.step(); });
+        }
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            ub[4 * j + 0] += sum_bits(fma2(g2.C, QS[b], MM));
-            ub[4 * j + 1] += sum_bits(fma2(g2.S, QS[b], MM));
-            ub[4 * j + 2] += sum_bits(fma2(g2.C, QI[b], MM));
-            ub[4 * j + 3] += sum_bits(fma2(g2.S, QI[b], MM));
-          }
+        for (int b = 0; b < NB; ++b) {
+          ub[4 * j + 0] += sum_bits(fma2(g2.C, QS[b], MM));
+          ub[4 * j + 1] += sum_bits(fma2(g2.S, QS[b], MM));
+          ub[4 * j + 2] += sum_bits(fma2(g2.C, QI[b], MM));
+          ub[4 * j + 3] += sum_bits(fma2(g2.S, QI[b], MM));
         }
       }
     }
-    st16(taddr + 16 * bt, ub);
   }
-  wait_st();
+  st16(taddr_bt, ub);
 }
 
 // v_row (bf_device.cuh) with the state in TMEM, one batch of four terms in registers at a time.
@@ -156,13 +155,17 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
         wait_ld();
       }
       if (i > 0) {
+        if (CONSEC) {
 #pragma unroll
-        for (int b = 0; b < NB; ++b) g2[b].step();
-        if (!CONSEC)
-          extra_steps(P.kstep[t0 + i], [&] {
+          for (int b = 0; b < NB; ++b) g2[b].step();
+        } else {   // k_i - k_{i-1} >= 1 steps as one loop (no separate paths for the gaps to merge)
+          int n = P.kstep[t0 + i];
+#pragma unroll 1
+          do {
 #pragma unroll
             for (int b = 0; b < NB; ++b) g2[b].step();
-          });
+          } while (--n > 0);
+        }
       }
       const int j = i & 3;
 #pragma unroll

@@ -96,9 +96,12 @@ constexpr int MBAR_BYTES = 64;
 #endif
 constexpr int W2_LAUNCH_REG = 80;   // registers per thread at launch (768 threads, one CTA per SM)
 constexpr int BAR_TM_DONE = 15;   // V warps: every TMEM access done (the allocating warp then frees)
-constexpr unsigned TM_COLS = 256;   // TMEM columns: 3 V warps per lane quarter x 64 (4 MAXK, MAXK <= 16)
+constexpr int BAR_INIT = 12;      // every warp: the band's initial vertical state is in TMEM
 
 // diagnostic builds only (tools/build_variant.py): drop one role's arithmetic, keep its barriers
+#ifndef BF_HALFSCAN
+#define BF_HALFSCAN 1
+#endif
 #ifndef BF_X_NOV
 #define BF_X_NOV 0
 #endif
@@ -147,9 +150,15 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   double2* lut64 = reinterpret_cast<double2*>(lut + 256);
   longlong2* red = reinterpret_cast<longlong2*>(smem_raw + P.r_off);              // [2][TW][2]: sum of the senders' (num_b, den_b)
 
-  const int tid = threadIdx.x;
+  // Warp roles by a host-built map (P.wmap: physical warp -> logical warp): the four SM
+  // sub-partitions (physical warp id mod 4) get equal shares of the roles' issue load, whatever part
+  // of the FH / V warps the strip width leaves idle. Everything below uses the logical thread id.
+  const int pw = (int)threadIdx.x >> 5;
+  const int tid = ((int)P.wmap[pw] << 5) | ((int)threadIdx.x & 31);
   const int G = CL ? P.G : 1;
-  const int rank = CL ? (int)cluster_rank() : 0;
+  // the CTA's rank in its (G, 1, 1) cluster, from blockIdx so that the compiler sees a warp-uniform
+  // value: the per-term branches on kval / kstep of this CTA's terms then run on the uniform datapath
+  const int rank = CL ? (int)(blockIdx.x % (unsigned)P.G) : 0;
   const int t0 = CL ? rank * P.tpc : 0;                      // this CTA's terms [t0, t0 + nkc)
   const int nkc = CL ? min(P.tpc, P.nk - t0) : P.nk;
   const int ngrp = (4 * nkc + 31) >> 5;
@@ -167,7 +176,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   fill_luts<U8>(P, lut, lut64, tid, NTH);
   __shared__ unsigned tmem_slot;
   if constexpr (TM) {
-    if (tid >= V0 && tid < V0 + 32) tm::alloc(&tmem_slot, TM_COLS);   // the first V warp allocates
+    if (tid >= V0 && tid < V0 + 32) tm::alloc(&tmem_slot, (unsigned)P.tmcols);   // the first V warp allocates
     tm::fence_before();
   }
   if constexpr (CL) {
@@ -184,7 +193,33 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
     __syncthreads();
   }
 
-  if constexpr (TM) tm::fence_after();
+  if constexpr (TM) {
+    // ---------------------------------------------------------- vertical state of the band's first row
+    // Every warp of the CTA takes part: the units (working V warp, column, batch of four terms) of
+    // a lane quarter are dealt round-robin to the six warps of that SM sub-partition (a warp
+    // reaches exactly its own quarter of TMEM), so the FH and S warps, idle until the first row
+    // arrives, halve the time before it.
+    tm::fence_after();
+    if (!BF_X_NOV) {
+      const int q = pw & 3;
+      const int nbt = FULL ? MAXK / 4 : (nkc + 3) >> 2;
+      const int upw = COLS * nbt, nun = (int)P.nvq[q] * upw;
+      const unsigned tq = tmem_slot + ((unsigned)(32 * q) << 16);
+      for (int u = pw >> 2; u < nun; u += NTH / 128) {
+        const int k = u / upw, r = u - k * upw, j = r / nbt, bt = r - j * nbt;
+        const int e = (((int)P.vq[q][k]) << 5 | ((int)threadIdx.x & 31)) + j * W2_V;   // extended column
+        if ((e & ~31) < wv) {
+          const int cj = x0 - P.rlo_x + e;
+          tm::v_init_batch<MAXK, NB, U8, CONSEC, FULL, CL>(P, in, lut, fbase, cj, (cj >= 0) & (cj < P.W) & (e < wv), y0, t0,
+                                                           nkc, bt, tq + (unsigned)((k * COLS + j) * 4 * MAXK + 16 * bt));
+        }
+      }
+      tm::wait_st();
+    }
+    tm::fence_before();
+    bar_sync(BAR_INIT, NTH);
+    tm::fence_after();
+  }
   if (tid >= V0) {
     // ------------------------------------------------------------ V role
     if constexpr (VREG > LREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(VREG));
@@ -200,22 +235,20 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       vwork[j] = ((vt & ~31) + j * W2_V) < wv;     // warp-uniform: this block of 32 columns is scanned
     }
     int U[TM ? 1 : COLS][TM ? 1 : NS * 4 * MAXK];
-    // TM: this thread's TMEM lane (its warp's lane quarter) and COLS x 4 MAXK columns (three V warps
-    // share a quarter; column j of the thread at + 4 MAXK j)
-    const unsigned taddr = TM ? tmem_slot + ((unsigned)(32 * ((tid >> 5) & 3)) << 16) +
-                                    (unsigned)(((tid - V0) >> 7) * COLS * 4 * MAXK)
+    // TM: this thread's TMEM lane (the lane quarter of its PHYSICAL warp) and COLS x 4 MAXK columns
+    // (the V warps of a quarter take consecutive blocks, P.tmblk; column j of the thread at + 4 MAXK j)
+    const unsigned taddr = TM ? tmem_slot + ((unsigned)(32 * (pw & 3)) << 16) +
+                                    (unsigned)((int)P.tmblk[pw] * COLS * 4 * MAXK)
                               : 0u;
     // prefetched taps: COLS == 1 the next row's; COLS == 2 the next (row, column) in the order
     // (y, 0), (y, 1), (y + 1, 0), ... (one column's worth of registers)
     float Ipre[NB][2];
+    if constexpr (!TM) {
 #pragma unroll
-    for (int j = 0; j < COLS; ++j)
-      if (vwork[j] && !BF_X_NOV) {
-        if constexpr (TM)
-          tm::v_init<MAXK, NB, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc,
-                                                     taddr + 4 * MAXK * j);
-        else v_init<MAXK, NB, NS, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, U[j]);
-      }
+      for (int j = 0; j < COLS; ++j)
+        if (vwork[j] && !BF_X_NOV)
+          v_init<MAXK, NB, NS, U8, CONSEC, FULL, CL>(P, in, lut, fbase, col[j], colok[j], y0, t0, nkc, U[j]);
+    }
     load_taps<NB, U8>(P, in, fbase, col[0], colok[0], y0, Ipre);
     for (int y = y0; y < yend; ++y) {
       const int b = (y - y0) & 1;
@@ -266,6 +299,9 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
               v_row<MAXK, NB, NS, U8, CONSEC, FULL, UP, GroupSync, CL>(P, lut, okj, y, t0, nkc, Icur, U[j],
                                                                       Ub + j * W2_V);
           }
+          // the first W2_V columns are written: the S warp scans them while the second column of
+          // every V thread is still being computed (barrier ids of group 1, unused with one group)
+          if (BF_HALFSCAN && j == 0) bar_arrive(BAR_U_FULL + 2 * b + 1, n_ufull);
         }
         hook.end(0);
       }
@@ -277,7 +313,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       tm::fence_before();
       bar_sync(BAR_TM_DONE, W2_V);
       tm::fence_after();
-      if (tid < V0 + 32) tm::dealloc(tmem_slot, TM_COLS);
+      if (tid < V0 + 32) tm::dealloc(tmem_slot, (unsigned)P.tmcols);
     }
   } else if (tid >= S0) {
     // ------------------------------------------------------------ S role: prefix scans
@@ -288,8 +324,18 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       const bool act = slot < 4 * nkc;
       for (int y = y0; y < yend; ++y) {
         const int b = (y - y0) & 1;
-        bar_sync(BAR_U_FULL + 2 * b + g, n_ufull);
-        if (act && !BF_X_NOS) prefix_row(Ubuf + b * srow + slot * UP, wv);
+        if (COLS == 2 && BF_HALFSCAN) {   // the row in two pieces, as the V threads' columns complete
+          int* Q = Ubuf + b * srow + slot * UP;
+          const int h = min(W2_V, wv);
+          int carry = 0;
+          bar_sync(BAR_U_FULL + 2 * b + 1, n_ufull);
+          if (act && !BF_X_NOS) carry = prefix_part(Q, 0, h, 0);
+          bar_sync(BAR_U_FULL + 2 * b, n_ufull);
+          if (act && !BF_X_NOS) Q[wv] = prefix_part(Q, h, wv, carry);
+        } else {
+          bar_sync(BAR_U_FULL + 2 * b + g, n_ufull);
+          if (act && !BF_X_NOS) prefix_row(Ubuf + b * srow + slot * UP, wv);
+        }
         bar_arrive(BAR_Q_FULL + 2 * b + g, n_qfull);
       }
     }
@@ -335,8 +381,13 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
           if (FULL || i < nkc) {
             if ((i & 7) == 0) bar_sync(BAR_Q_FULL + 2 * b + (i >> 3), n_qfull);
             if (!DUMP && i > 0 && !BF_X_NOW) {   // k_i - k_{i-1} >= 1 steps
-              gk.step();
-              if (!CONSEC) extra_steps(P.kstep[t0 + i], [&] { gk.step(); });
+              if (CONSEC) gk.step();
+              else {
+                int n = P.kstep[t0 + i];
+#pragma unroll 1
+                do gk.step();
+                while (--n > 0);
+              }
             }
             int h0[4], h1[4];
 #pragma unroll

@@ -14,6 +14,9 @@ def pytest_configure(config):
 
 
 def pytest_collection_modifyitems(config, items):
+    # the every-pixel full-size parity tests take minutes of oracle time each: run them after every
+    # other test, so that a time limit on the whole suite cuts them and not the rest
+    items.sort(key=lambda it: "test_gpu_fullsize" in it.nodeid)
     try:
         import torch
         has_gpu = torch.cuda.is_available()

@@ -168,6 +168,28 @@ def test_launch_config_query(bfmod):
         assert tw == widest or (tw % 32 == 0 and 128 <= tw < widest), (cfg, tw)
         if cluster > 1:
             assert c["terms_per_cta"] * cluster >= len(plan.info()["k"]) > c["terms_per_cta"] * (cluster - 1)
+        # warp roles: a permutation of the 24 logical warps. The WORKING warps of each role (FH: one
+        # per 32 output columns, S: one per 32-channel group, V: one per 32 extended columns) are
+        # placed over the four SM sub-partitions (physical warp mod 4) by the rule the on-GPU search
+        # found (bf_apply.cu, ws2_warp_map): the S warps share one sub-partition, the FH warps are
+        # spread evenly over the other three, the V warps evenly over all four
+        m = c["warp_map"]
+        assert sorted(m) == list(range(24)), (cfg, m)
+        nfh, ns = (10, 2) if cols == 1 else (11, 1)
+        nk = min(c["terms_per_cta"], len(plan.info()["k"]))
+        wv = (tw + halo + 7) // 8 * 8
+        ngrp = (4 * nk + 31) // 32
+        fq, sq, vq = [0] * 4, [0] * 4, [0] * 4
+        for pw, l in enumerate(m):
+            if l < nfh:
+                fq[pw % 4] += 32 * l < tw
+            elif l < nfh + ns:
+                sq[pw % 4] += l - nfh < ngrp
+            else:
+                vq[pw % 4] += 32 * (l - nfh - ns) < wv
+        assert sorted(sq) == [0, 0, 0, min(ns, ngrp)], (cfg, sq)
+        others = [fq[q] for q in range(4) if sq[q] == 0]
+        assert max(others) - min(others) <= 1 and max(vq) - min(vq) <= 1, (cfg, fq, vq)
     spec = CONFIGS["cfg2"]
     p = config_params(spec)
     plan = bfmod.Plan(spatial=p["spatial"], range_kind=p["range_kind"], sigma_s=p["sigma_s"], sigma_r=p["sigma_r"],
