@@ -184,14 +184,28 @@ struct Rot2 {
     if ((k0 & (k0 - 1)) == 0) {
       // k0 = 2^m (the cluster split's first terms, 8 and 16): the general loop below reduces to m
       // squarings of (c1, s1) with the same operations; without its per-bit bookkeeping
+      // (k0 = 8 and 16 as straight-line code: the loop's counter, branches and register moves
+      // were a tenth of the two-column V role's instructions)
       u64 bc = C1, bs = S1;
-#pragma unroll 1
-      for (int k = k0; k > 1; k >>= 1) {
+      auto square = [&] {
         const u64 nbs = bs ^ 0x8000000080000000ull;
         const u64 bcn = fma2(bs, nbs, mul2(bc, bc));
         const u64 bsn = fma2(bc, bs, mul2(bs, bc));
         bc = bcn;
         bs = bsn;
+      };
+      if (k0 == 8) {
+        square();
+        square();
+        square();
+      } else if (k0 == 16) {
+        square();
+        square();
+        square();
+        square();
+      } else {
+#pragma unroll 1
+        for (int k = k0; k > 1; k >>= 1) square();
       }
       C = bc;
       S = bs;
@@ -490,8 +504,12 @@ __device__ __forceinline__ void v_row(const KParams& P, const float2* lut, bool 
 // IADD3 per column); int32 wrap-around keeps every box difference exact. Q[n] = total.
 // prefix_part scans columns [e0, e1) with the running total carried in and returned (a row scanned
 // in pieces, as its columns become available, equals the row scanned at once).
+#ifndef BF_SCAN_UNROLL
+#define BF_SCAN_UNROLL 8
+#endif
+constexpr int SCAN_UNROLL = BF_SCAN_UNROLL;
 __device__ __forceinline__ int prefix_part(int* Q, int e0, int e1, int carry) {
-#pragma unroll 8
+#pragma unroll SCAN_UNROLL
   for (int e = e0; e < e1; e += 8) {
     const int4 a = *reinterpret_cast<const int4*>(Q + e), b = *reinterpret_cast<const int4*>(Q + e + 4);
     const int o1 = carry + a.x;

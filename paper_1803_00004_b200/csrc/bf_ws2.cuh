@@ -99,6 +99,9 @@ constexpr int BAR_TM_DONE = 15;   // V warps: every TMEM access done (the alloca
 constexpr int BAR_INIT = 12;      // every warp: the band's initial vertical state is in TMEM
 
 // diagnostic builds only (tools/build_variant.py): drop one role's arithmetic, keep its barriers
+#ifndef BF_S_REG
+#define BF_S_REG 0   // S role registers (0 = default 48 / 56)
+#endif
 #ifndef BF_HALFSCAN
 #define BF_HALFSCAN 1
 #endif
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   //          two columns: V 384 x 80 + FH 352 x 80 + S 32 x 48 = 60416 (cfg4 32.2 ms; 37.3 at 64)
   //   else   V 384 x 112 + (FH + S) 384 x 48      = 61440
   constexpr int VREG = TM ? (COLS == 2 ? BF_TM_VREG2 : BF_TM_VREG) : (NPL > 1 ? 104 : 112);
-  constexpr int OREG = NPL > 1 ? 56 : 48;
+  constexpr int OREG = BF_S_REG ? BF_S_REG : (NPL > 1 ? 56 : 48);
   constexpr int FHREG = TM ? BF_TM_FHREG : OREG;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem_raw);   // FULL[2], EMPTY[2]
