@@ -376,6 +376,9 @@ bf_status repair_sink(const bf_apply_args& A, double wscale, double mfull, doubl
 #ifndef BF_WMAP
 #define BF_WMAP 1
 #endif
+#ifndef BF_INIT_SCALE
+#define BF_INIT_SCALE 1.0   // cost-model weight of a row of the band's initial state
+#endif
 #ifndef BF_MINTH
 #define BF_MINTH 4   // least band height of kernel 2b (cfg0 at 16: 0.048 ms, at 4: 0.026 ms)
 #endif
@@ -536,7 +539,7 @@ size_t smem_ws2(int cols, int nkc, int tw, int G, bool u8, int& l_off, int& r_of
   l_off = (int)off;
   if (u8) off += 256 * (sizeof(float2) + sizeof(double2));
   r_off = (int)off;
-  if (G > 1) off += 2 * (size_t)tw * 2 * sizeof(longlong2);   // per row parity: sum of the senders' (num_b, den_b)
+  if (G > 1) off += W2_XSLOTS * (size_t)tw * 2 * sizeof(longlong2);   // per row slot: sum of the senders' (num_b, den_b)
   return off;
 }
 
@@ -637,7 +640,7 @@ bf_status prepare(const Req& R, const bf_plan* p, Launch& L) {
         // measured ~0.55 IPC per SM sub-partition, never below one warp's dependent chain
         const double row = std::max(6000.0 * ch, ch * (694.0 * ((wv + 31) / 32) + 942.0 * ((tw + 31) / 32) + 4.0 * wv) /
                                                      (4 * 0.55));
-        const double init = std::max(1500.0 * ch, ch * 373.0 * ((wv + 31) / 32) / (4 * 0.55));
+        const double init = BF_INIT_SCALE * std::max(1500.0 * ch, ch * 373.0 * ((wv + 31) / 32) / (4 * 0.55));
         const long long strips = (W + tw - 1) / tw;
         const int slots = G > 1 ? max_clusters(s, smem, G) : nsm;   // resident clusters (CTAs for G = 1)
         for (int nb = 1; nb <= Hr; ++nb) {

@@ -96,6 +96,13 @@ struct LaunchSpec {
 
 constexpr int KERN_BAND = 0, KERN_WS = 1, KERN_WS2 = 2;
 
+// kernel 2b cluster split: row slots of the DSMEM exchange (the senders may run this many rows
+// ahead of CTA 0's consumption)
+#ifndef BF_XSLOTS
+#define BF_XSLOTS 2
+#endif
+constexpr int W2_XSLOTS = BF_XSLOTS;
+
 // kernel 2 (bf_ws_kernel) role sizes
 constexpr int WS_V = 256, WS_S = 64, WS_F = 192, WS_C = 128, WS_THREADS = WS_V + WS_S + WS_F + WS_C;
 constexpr int WS_H = WS_S + WS_F;

@@ -119,7 +119,7 @@ constexpr int BAR_INIT = 12;      // every warp: the band's initial vertical sta
 #endif
 #ifndef BF_X_NOLDS
 #define BF_X_NOLDS 0
-#endif   // mbarriers at the start of shared memory (FULL[2], EMPTY[2])
+#endif   // mbarriers at the start of shared memory (FULL[XS], EMPTY[XS])
 
 template <int MAXK, int FORM, bool U8, bool CONSEC, bool FULL, int NPL, int COLS, bool CL, bool DUMP>
 __global__ void __launch_bounds__(W2_THREADS, 1)
@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   constexpr int H0 = 0, S0 = NFH, V0 = NFH + NSW;
   static_assert(V0 + W2_V == NTH, "role sizes");
   constexpr int LREG = W2_LAUNCH_REG;
+  constexpr int XS = W2_XSLOTS;   // row slots of the cluster exchange
   constexpr int UP = w2_up(COLS);
   constexpr bool PB = NPL == 1 && !DUMP;   // per-box accumulators (see the FH role)
   // TM: the V role's sliding sums in tensor memory (bf_tm.cuh; one column per V thread), which
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   constexpr int OREG = BF_S_REG ? BF_S_REG : (NPL > 1 ? 56 : 48);
   constexpr int FHREG = TM ? BF_TM_FHREG : OREG;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem_raw);   // FULL[2], EMPTY[2]
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem_raw);   // FULL[XS], EMPTY[XS]
   int* Ubuf = reinterpret_cast<int*>(smem_raw + MBAR_BYTES);                     // [2][4 nk][UP]
   float2* lut = reinterpret_cast<float2*>(smem_raw + P.l_off);
   double2* lut64 = reinterpret_cast<double2*>(lut + 256);
@@ -184,13 +185,13 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   }
   if constexpr (CL) {
     if (tid == 0) {
-      mbar_init(smem_u32(&mbar[0]), 1);           // FULL[b]: CTA 0's expect_tx arrival + the senders' bytes
-      mbar_init(smem_u32(&mbar[1]), 1);
-      mbar_init(smem_u32(&mbar[2]), NFH / 32);    // EMPTY[b]: every FH warp of CTA 0 once per row
-      mbar_init(smem_u32(&mbar[3]), NFH / 32);
+      for (int i = 0; i < XS; ++i) {
+        mbar_init(smem_u32(&mbar[i]), 1);               // FULL[slot]: CTA 0's expect_tx arrival + the senders' bytes
+        mbar_init(smem_u32(&mbar[XS + i]), NFH / 32);   // EMPTY[slot]: every FH warp of CTA 0 once per row
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = tid; i < 2 * 2 * P.TW; i += NTH) red[i] = make_longlong2(0, 0);   // both slots
+    for (int i = tid; i < XS * 2 * P.TW; i += NTH) red[i] = make_longlong2(0, 0);   // every slot
     cluster_sync();
   } else {
     __syncthreads();
@@ -465,14 +466,15 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       }
       if constexpr (DUMP) continue;
       if constexpr (CL) {
-        const unsigned ph = ((y - y0) >> 1) & 1;
+        const int xb = (y - y0) % XS;                        // exchange slot of this row
+        const unsigned ph = (unsigned)((y - y0) / XS) & 1;
         if (rank > 0) {
-          // sender: wait until CTA 0 has consumed row y - 2 from slot b, then store the partials
+          // sender: wait until CTA 0 has consumed row y - XS from the slot, then store the partials
           if (wact) {
-            if (y - y0 >= 2) mbar_wait(smem_u32(&mbar[2 + b]), ph ^ 1);
+            if (y - y0 >= XS) mbar_wait(smem_u32(&mbar[XS + xb]), ph ^ 1);
             if (act) {
-              const unsigned dst = map_rank(red_l + (unsigned)((b * P.TW + o) * 32), 0);
-              const unsigned fb = map_rank(full_l + 8 * b, 0);
+              const unsigned dst = map_rank(red_l + (unsigned)((xb * P.TW + o) * 32), 0);
+              const unsigned fb = map_rank(full_l + 8 * xb, 0);
               red_async_add(dst, num[0], fb);
               red_async_add(dst + 8, den[0], fb);
               red_async_add(dst + 16, num[1], fb);
@@ -480,14 +482,14 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
             }
           }
         } else {
-          if (o == 0) mbar_expect(full_l + 8 * b, (unsigned)((G - 1) * TWv * 32));
+          if (o == 0) mbar_expect(full_l + 8 * xb, (unsigned)((G - 1) * TWv * 32));
           if (wact) {
-            mbar_wait(full_l + 8 * b, ph);
+            mbar_wait(full_l + 8 * xb, ph);
             if (act) {
               // the senders' partials, added exactly in CTA 0's slot (integer adds: any order)
-              longlong2* r2 = red + 2 * (b * P.TW + o);
+              longlong2* r2 = red + 2 * (xb * P.TW + o);
               const longlong2 v0 = r2[0], v1 = r2[1];
-              r2[0] = make_longlong2(0, 0);   // cleared for row y + 2 (ordered before the release below)
+              r2[0] = make_longlong2(0, 0);   // cleared for row y + XS (ordered before the release below)
               r2[1] = make_longlong2(0, 0);
               num[0] += v0.x;
               den[0] += v0.y;
@@ -498,7 +500,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
           }
           __syncwarp();
           if ((tid & 31) == 0)
-            for (int s = 1; s < G; ++s) mbar_arrive_remote(map_rank(smem_u32(&mbar[2 + b]), s));
+            for (int s = 1; s < G; ++s) mbar_arrive_remote(map_rank(smem_u32(&mbar[XS + xb]), s));
         }
       } else if constexpr (PB) {
         if (act) finish_pixel_pb(P, num, den, ax0, ax1, Ic, prow + (long long)y * P.W, out, hm0, hm1, ws);
