@@ -1113,7 +1113,10 @@ unsigned long long spatial_key(const bf_plan* p) {
 }
 
 // ---- bf_apply_host: device buffers, streams and events per device
-constexpr int HOST_CHUNKS = 5;
+#ifndef BF_HOST_CHUNKS
+#define BF_HOST_CHUNKS 5
+#endif
+constexpr int HOST_CHUNKS = BF_HOST_CHUNKS;
 struct HostCache {
   std::mutex mu;
   bool ready = false;

@@ -153,6 +153,22 @@ def test_degenerate_shapes(gpu, H, W):
     assert_parity(run_gpu(pkg, torch, gp, img), bf.bf_box(img, op), 255.0, f"{H}x{W}")
 
 
+@pytest.mark.parametrize("cfg,W", [("cfg0", 40), ("cfg0", 100), ("cfg0", 170), ("cfg3", 230), ("cfg1", 75),
+                                   ("cfg1", 140), ("cfg1", 290), ("cfg2", 150)])
+def test_strip_widths_and_warp_role_maps(gpu, cfg, W):
+    """Strips that leave different numbers of FH / V warps working (kernel 2b's warp-role map,
+    the per-sub-partition deal of the band's initial state and the TMEM blocks all depend on
+    them): whole image against the oracle, and the map a permutation of the 24 warps."""
+    pkg, torch = gpu
+    spec = CONFIGS[cfg]
+    H = 70
+    img = config_input(spec, H=H, W=W)
+    gp, op = make_plans(pkg, config_params(spec), img.dtype)
+    c = pkg.config(gp, H, W)
+    assert c["kernel"] == "bf_ws2_kernel" and sorted(c["warp_map"]) == list(range(24)), c
+    assert_parity(run_gpu(pkg, torch, gp, img), bf.bf_box(img, op), spec.intensity_max, f"{cfg} W={W}")
+
+
 def test_constant_image(gpu):
     pkg, torch = gpu
     img = np.full((70, 90), 0.625, dtype=np.float32)
