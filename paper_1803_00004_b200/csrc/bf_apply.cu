@@ -376,6 +376,9 @@ bf_status repair_sink(const bf_apply_args& A, double wscale, double mfull, doubl
 #ifndef BF_WMAP
 #define BF_WMAP 1
 #endif
+#ifndef BF_TW_FORCE
+#define BF_TW_FORCE 0
+#endif
 #ifndef BF_INIT_SCALE
 #define BF_INIT_SCALE 1.0   // cost-model weight of a row of the band's initial state
 #endif
@@ -631,6 +634,7 @@ bf_status prepare(const Req& R, const bf_plan* p, Launch& L) {
       const double ch = 4.0 * nkc / 64.0;
       for (int tw = twmax; tw >= 1; tw = (tw % 32) ? tw - tw % 32 : tw - 32) {
         if (tw != twmax && tw < 128) break;
+        if (BF_TW_FORCE && cols == 2 && tw != BF_TW_FORCE) continue;   // A/B builds only
         int lo, ro;
         const size_t smem = smem_ws2(cols, nkc, tw, G, u8, lo, ro);
         if (smem > 227 * 1024) continue;
