@@ -49,9 +49,10 @@ def layouts(counts):
         yield sub
 
 
-def build_map(sub, classes, idle, order):
+def build_map(sub, classes, idle, order, idle_at=None):
     """sub: per sub-partition the counts per class; classes: logical warps of each class (working);
-    idle: idle logical warps; order: class order inside a sub-partition."""
+    idle: idle logical warps; order: class order inside a sub-partition; idle_at: position of the
+    idle warps in a sub-partition's slot sequence (None = last)."""
     pools = [list(c) for c in classes]
     idle = list(idle)
     m = [0] * 24
@@ -61,7 +62,10 @@ def build_map(sub, classes, idle, order):
             for _ in range(sub[q][ci]):
                 seq.append(pools[ci].pop(0))
         while len(seq) < 6:
-            seq.append(idle.pop(0))
+            if idle_at is None:
+                seq.append(idle.pop(0))
+            else:
+                seq.insert(min(idle_at, len(seq)), idle.pop(0))
         for i, l in enumerate(seq):
             m[q + 4 * i] = l
     return m
@@ -147,10 +151,11 @@ def main():
         best = []
         for t, sub in res[:6]:
             for order in ((0, 1, 2, 3), (1, 0, 2, 3), (2, 3, 1, 0), (2, 3, 0, 1), (1, 2, 3, 0)):
-                m = build_map(sub, classes, idle, order)
-                t2 = time_map(m, 4 * n1)
-                assert torch.equal(y, ref), "a warp map changed the output"
-                best.append((t2, sub, order, m))
+                for idle_at in (None, 0, 2):
+                    m = build_map(sub, classes, idle, order, idle_at)
+                    t2 = time_map(m, 4 * n1)
+                    assert torch.equal(y, ref), "a warp map changed the output"
+                    best.append((t2, sub, (order, idle_at), m))
         best.sort(key=lambda r: r[0])
         print(f"{cfg} second pass:")
         for t2, sub, order, m in best[:10]:
