@@ -8,7 +8,11 @@
 //                      the pixel's fp64 combine weights (per range plan for bf_apply_multi)
 //   S   next warps     warp g turns group g's U' rows into exclusive prefix rows Q in place
 //   V   last 12 warps  COLS extended columns per thread: slides the vertical sums, writes U'(y)
-// FH has the lowest warp ids (the schedulers favour older warps; FH is the critical role).
+// These are LOGICAL warp ids: the host maps them onto the physical warps (KParams::wmap, built by
+// ws2_warp_map in bf_apply.cu from a measured placement rule) so that the S warps share one SM
+// sub-partition and the working FH / V warps are spread evenly over the four; within a
+// sub-partition the V warps take the lowest physical ids. Before the first row every warp, whatever
+// its role, computes part of the band's initial vertical state (tm::v_init_batch).
 //
 // COLS = 2 (wide radii, e.g. cfg4's r = 192): each V thread keeps the vertical state of two
 // columns 384 apart, so a strip covers 768 extended columns (output strip 352 wide instead of
